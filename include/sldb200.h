@@ -1,0 +1,164 @@
+/*
+ * sldb200.h -- C ABI of the B200 Krylov SpMV engine (libsldb200.so).
+ *
+ * The drop-in boundary for the reference's block-Wiedemann hot path
+ * (arxiv/paper_1402_3661, Python package `sldlag`).  The reference has no
+ * native code and no FFI; its plugin seam is the duck-typed *multiplier*
+ * protocol (`.apply(planes) -> planes`, `.count`, `.size`, `.mod`,
+ * sldlag/solver.py:129-163) plus the projection protocol
+ * (`.project(planes) -> list[int]`, solver.py:168-189).  Every entry point
+ * below replaces one piece of that Python path; the ctypes binding a
+ * maintainer adds on the reference side is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Plain C types only; no torch types.  Every function returns 0 on
+ *     success or a negative SLD_E* code; sld_last_error() gives a
+ *     thread-local message for the last failure on the calling thread.
+ *   - Residues cross the ABI either as the reference's "digit planes"
+ *     (row-major N x P uint64 cells each holding one little-endian 16-bit
+ *     digit, P = ceil(bits(l)/16); sldlag/vecops.py:22-47) or as
+ *     little-endian 32-bit limbs (N x L uint32, L = ceil(bits(l)/32)).
+ *     Values are canonical residues in [0, l) on both sides; results are
+ *     bit-identical to the reference's (integers, not representations).
+ *   - Handles are opaque and owned by the caller (free with *_destroy).
+ *     One sld_ctx = one CUDA device + one stream; a context must not be
+ *     used from two host threads at once (the reference runs one
+ *     multiplier per chain thread, solver.py:249-251 -- create one context
+ *     per thread/device).  All calls release no locks of their own and are
+ *     safe to call with the Python GIL released (ctypes does).
+ */
+#ifndef SLDB200_H
+#define SLDB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLD_OK 0
+#define SLD_E_ARG -1     /* bad argument / shape  (reference: ValueError)      */
+#define SLD_E_CUDA -2    /* CUDA runtime failure  (reference: n/a)             */
+#define SLD_E_BOUND -3   /* exactness bound exceeded (reference: AssertionError,
+                            vecops.py:407,414 / ContractViolation modring.py:40) */
+#define SLD_E_NCCL -4    /* collective failure                                 */
+
+typedef struct sld_ctx sld_ctx;
+typedef struct sld_mat sld_mat;
+typedef struct sld_vec sld_vec;
+
+/* library / error plumbing */
+int sld_version(void);
+const char *sld_last_error(void);
+int sld_device_count(int *out);
+
+/*
+ * Field context: one prime l on one device.  Replaces PrimeModulus as the
+ * object that crosses every API (sldlag/modring.py:44-130).  ell_limbs: the
+ * prime as L little-endian 32-bit words (l odd, 3 <= l, bits(l) <= 1024).
+ */
+int sld_ctx_create(int device, const uint32_t *ell_limbs, int L, sld_ctx **out);
+int sld_ctx_destroy(sld_ctx *ctx);
+int sld_ctx_sync(sld_ctx *ctx);
+
+/*
+ * Matrix upload + GPU layout build.  Replaces SparseMatrix.kernel() /
+ * SpmvKernel.__init__ (sldlag/spmatrix.py:205-230, vecops.py:366-414).
+ * Inputs mirror the SparseMatrix fields (spmatrix.py:77-91):
+ *   row_ptr[nrows+1] (int64), col_idx[nnz] (int32 sparse column < ncols),
+ *   tags[nnz] (0:+1, 1:-1, 2:small, 3:full -- modring.py:26-29),
+ *   small_vals[nnz] (int64; read for tag 2; |c| >= 2^31 is promoted to the
+ *   full class, value c mod l, exactly the "smallest class" rule of
+ *   spmatrix.py:48-66 run in reverse),
+ *   n_full entries at sorted flat positions full_pos[] with values
+ *   full_limbs[n_full*L] (canonical), and n_dense dense columns
+ *   dense_limbs[n_dense*nrows*L] occupying global columns ncols..ncols+n_dense-1
+ *   (spmatrix.py:69-75; zero entries allowed).
+ * max_stripe_cols: column-stripe width for L2 residency of the gathered
+ *   vector (0 = automatic, from the device's L2 size).
+ * Errors: SLD_E_ARG for inconsistent CSR (spmatrix.py:93-126 checks),
+ * SLD_E_BOUND if a row has more than 2^15 small-class or 2^24 +-1 entries.
+ */
+int sld_mat_create(sld_ctx *ctx, int64_t nrows, int64_t ncols,
+                   const int64_t *row_ptr, const int32_t *col_idx,
+                   const uint8_t *tags, const int64_t *small_vals,
+                   int64_t n_full, const int64_t *full_pos, const uint32_t *full_limbs,
+                   int n_dense, const uint32_t *dense_limbs,
+                   int64_t max_stripe_cols, sld_mat **out);
+int sld_mat_destroy(sld_mat *m);
+/* info[0..15]: nrows, total_cols, nnz, n_pm, n_small, n_full(+dense nz),
+ * stripes, nslices, device bytes, padded index entries, L, stride words,
+ * max row degree, 0, 0, 0 */
+int sld_mat_info(const sld_mat *m, int64_t *info);
+
+/*
+ * Device vectors of `n` residues (n = total_cols of the matrices they feed).
+ * Upload/download accept the reference's digit planes (vecops.py:35-47) or
+ * 32-bit limbs; planes are repacked on the device.
+ */
+int sld_vec_create(sld_ctx *ctx, int64_t n, sld_vec **out);
+int sld_vec_destroy(sld_vec *v);
+int sld_vec_upload_planes(sld_vec *v, const uint64_t *planes, int64_t n, int P);
+int sld_vec_download_planes(sld_vec *v, uint64_t *planes, int64_t n, int P);
+int sld_vec_upload_limbs(sld_vec *v, const uint32_t *limbs, int64_t n);
+int sld_vec_download_limbs(sld_vec *v, uint32_t *limbs, int64_t n);
+/* raw device pointer + stride (words) -- for collectives and tests */
+int sld_vec_device_ptr(sld_vec *v, uint64_t *ptr, int64_t *stride_words);
+
+/*
+ * out = A * in (mod l), canonical.  Replaces SpmvKernel.apply
+ * (vecops.py:428-470) and spmv_planes (spmatrix.py:242-246); `in` must
+ * have total_cols residues and `out` nrows residues (and be distinct).
+ */
+int sld_spmv(sld_mat *m, sld_vec *in, sld_vec *out);
+
+/* Host-buffer convenience: planes in, planes out (the multiplier's
+ * `.apply(planes)` contract, solver.py:140-142). */
+int sld_spmv_planes(sld_mat *m, const uint64_t *in_planes, uint64_t *out_planes, int P);
+
+/*
+ * Device-resident Krylov chain.  Replaces the loop of krylov_column
+ * (solver.py:199-217) with UnitRows projections (solver.py:174-176):
+ * for i in [0, steps): terms[i] = X^T v; v = A v.
+ *   v: in/out iterate (total_cols == nrows, square matrix).
+ *   x_rows[m]: unit projection rows.  terms_limbs: steps*m*L uint32
+ *   (host), term i / column t at (i*m + t)*L.
+ * Steps run as CUDA-graph chunks; the call returns after `steps` products.
+ */
+int sld_krylov_unit(sld_mat *m, sld_vec *v, const int64_t *x_rows, int mrows,
+                    int64_t steps, uint32_t *terms_limbs);
+
+/*
+ * Same with a dense X block (DenseRows.project, solver.py:186-189):
+ * x: an (mrows x total_cols) set of residues uploaded once with
+ * sld_xblock_create; terms[i][t] = sum_j x[t][j] v_i[j] mod l.
+ */
+typedef struct sld_xblock sld_xblock;
+int sld_xblock_create(sld_ctx *ctx, const uint32_t *x_limbs, int mrows, int64_t n, sld_xblock **out);
+int sld_xblock_destroy(sld_xblock *x);
+int sld_krylov_dense(sld_mat *m, sld_vec *v, sld_xblock *x, int64_t steps, uint32_t *terms_limbs);
+
+/*
+ * Timing hook for bench.py: runs `steps` products v <- A v on device
+ * (ping-pong, graph-captured) and returns device milliseconds measured
+ * with CUDA events on the context stream; kernel_ms gets the average
+ * duration of one product (all stripe passes).
+ */
+int sld_bench_spmv(sld_mat *m, sld_vec *v, int64_t steps, int warmup, double *total_ms,
+                   double *kernel_ms);
+
+/* Synthetic corpus generator (fixture producer, not timed): a native
+ * restatement of the row/column distribution of sldlag/corpus.py:104-139
+ * (row weight rint(N(gamma, 0.1 gamma)) clipped to [3, ncols/2], column j
+ * with probability ~ (j+1)^-decay, distinct sorted columns, +-1 with
+ * probability pm1, else a small coefficient of magnitude uniform in
+ * [2, cmax) with random sign).  Two-phase: count (row_ptr) then fill. */
+int sld_corpus_rows(int64_t n, int64_t ncols, double gamma, uint64_t seed, int64_t *row_ptr);
+int sld_corpus_fill(int64_t n, int64_t ncols, double decay, double pm1, int64_t cmax,
+                    uint64_t seed, const int64_t *row_ptr, int32_t *col_idx, uint8_t *tags,
+                    int64_t *small_vals, int nthreads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLDB200_H */

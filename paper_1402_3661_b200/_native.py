@@ -1,0 +1,134 @@
+"""ctypes binding of libsldb200.so (include/sldb200.h).
+
+The product path is Python -> ctypes -> CUDA.  There is no CPU fallback:
+if the shared library is missing or no CUDA device is visible, every call
+that needs the device raises `NativeUnavailable` (a RuntimeError).
+"""
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import _build
+
+LIB_PATH = _build.LIB
+
+SLD_OK = 0
+SLD_E_ARG = -1
+SLD_E_CUDA = -2
+SLD_E_BOUND = -3
+SLD_E_NCCL = -4
+
+# every symbol include/sldb200.h declares (checked by tests/test_native_abi.py)
+EXPORTS = [
+    "sld_version", "sld_last_error", "sld_device_count",
+    "sld_ctx_create", "sld_ctx_destroy", "sld_ctx_sync",
+    "sld_mat_create", "sld_mat_destroy", "sld_mat_info",
+    "sld_vec_create", "sld_vec_destroy", "sld_vec_upload_planes", "sld_vec_download_planes",
+    "sld_vec_upload_limbs", "sld_vec_download_limbs", "sld_vec_device_ptr",
+    "sld_spmv", "sld_spmv_planes", "sld_krylov_unit",
+    "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
+    "sld_bench_spmv", "sld_corpus_rows", "sld_corpus_fill",
+]
+
+
+class NativeUnavailable(RuntimeError):
+    """libsldb200.so could not be loaded or no CUDA device is usable."""
+
+
+class BoundError(AssertionError):
+    """Exactness bound exceeded (the reference raises AssertionError /
+    ContractViolation for the same condition, vecops.py:407,414)."""
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(build_if_missing=False):
+    """Load the shared library (raises NativeUnavailable if absent)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            if build_if_missing:
+                _build.build()
+            else:
+                raise NativeUnavailable(
+                    f"{LIB_PATH} is missing; build it with `python -m paper_1402_3661_b200._build` "
+                    "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32, u64p = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+        pp = ctypes.POINTER(ctypes.c_void_p)
+        sig = {
+            "sld_version": ([], i32),
+            "sld_last_error": ([], ctypes.c_char_p),
+            "sld_device_count": ([vp], i32),
+            "sld_ctx_create": ([i32, vp, i32, pp], i32),
+            "sld_ctx_destroy": ([vp], i32),
+            "sld_ctx_sync": ([vp], i32),
+            "sld_mat_create": ([vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, i32, vp, i64, pp], i32),
+            "sld_mat_destroy": ([vp], i32),
+            "sld_mat_info": ([vp, vp], i32),
+            "sld_vec_create": ([vp, i64, pp], i32),
+            "sld_vec_destroy": ([vp], i32),
+            "sld_vec_upload_planes": ([vp, u64p, i64, i32], i32),
+            "sld_vec_download_planes": ([vp, u64p, i64, i32], i32),
+            "sld_vec_upload_limbs": ([vp, vp, i64], i32),
+            "sld_vec_download_limbs": ([vp, vp, i64], i32),
+            "sld_vec_device_ptr": ([vp, vp, vp], i32),
+            "sld_spmv": ([vp, vp, vp], i32),
+            "sld_spmv_planes": ([vp, vp, vp, i32], i32),
+            "sld_krylov_unit": ([vp, vp, vp, i32, i64, vp], i32),
+            "sld_xblock_create": ([vp, vp, i32, i64, pp], i32),
+            "sld_xblock_destroy": ([vp], i32),
+            "sld_krylov_dense": ([vp, vp, vp, i64, vp], i32),
+            "sld_bench_spmv": ([vp, vp, i64, i32, vp, vp], i32),
+            "sld_corpus_rows": ([i64, i64, ctypes.c_double, ctypes.c_uint64, vp], i32),
+            "sld_corpus_fill": ([i64, i64, ctypes.c_double, ctypes.c_double, i64, ctypes.c_uint64,
+                                 vp, vp, vp, vp, i32], i32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return _lib
+
+
+def check(rc):
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == SLD_OK:
+        return
+    msg = load().sld_last_error().decode(errors="replace")
+    if rc == SLD_E_ARG:
+        raise ValueError(msg)
+    if rc == SLD_E_BOUND:
+        raise BoundError(msg)
+    raise RuntimeError(f"libsldb200: {msg}")
+
+
+def device_count():
+    n = ctypes.c_int(0)
+    rc = load().sld_device_count(ctypes.byref(n))
+    if rc != SLD_OK:
+        return 0
+    return n.value
+
+
+def ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None and a.size else ctypes.c_void_p(0)
+
+
+def c64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def c32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def cu32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)

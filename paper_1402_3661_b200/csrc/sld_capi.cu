@@ -1,0 +1,1104 @@
+// sld_capi.cu -- host side of libsldb200.so: the C ABI declared in
+// include/sldb200.h (matrix builder, vectors, SpMV and the device-resident
+// Krylov loop with CUDA graphs).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/sldb200.h"
+#include "sld_device.cuh"
+#include "sld_dense.cuh"
+
+using namespace sld;
+
+// ------------------------------------------------------------ errors
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                 \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(SLD_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                           \
+  } while (0)
+
+#define TRY(expr)              \
+  do {                         \
+    int r_ = (expr);           \
+    if (r_ != SLD_OK) return r_; \
+  } while (0)
+
+extern "C" const char* sld_last_error(void) { return g_err.c_str(); }
+extern "C" int sld_version(void) { return 1; }
+extern "C" int sld_device_count(int* out) {
+  CU(cudaGetDeviceCount(out));
+  return SLD_OK;
+}
+
+// ------------------------------------------------- host multiprecision
+
+// r = r*2 mod ell (r < ell), L words
+static void hmod_double(uint32_t* r, const uint32_t* ell, int L) {
+  uint32_t c = 0;
+  std::vector<uint32_t> t(L + 1);
+  for (int i = 0; i < L; i++) {
+    t[i] = (r[i] << 1) | c;
+    c = r[i] >> 31;
+  }
+  t[L] = c;
+  // t >= ell ?
+  bool ge = t[L] != 0;
+  if (!ge) {
+    ge = true;
+    for (int i = L - 1; i >= 0; i--)
+      if (t[i] != ell[i]) { ge = t[i] > ell[i]; break; }
+  }
+  if (ge) {
+    int64_t br = 0;
+    for (int i = 0; i < L; i++) {
+      int64_t v = (int64_t)t[i] - ell[i] + br;
+      t[i] = (uint32_t)v;
+      br = v >> 32;
+    }
+  }
+  for (int i = 0; i < L; i++) r[i] = t[i];
+}
+
+static int bitlen(const uint32_t* a, int n) {
+  while (n > 0 && a[n - 1] == 0) n--;
+  if (!n) return 0;
+  return 32 * (n - 1) + (32 - __builtin_clz(a[n - 1]));
+}
+
+// (|c| mod ell) for a 64-bit magnitude, L words out
+static void hmod_u64(uint64_t c, const uint32_t* ell, int L, uint32_t* out) {
+  std::vector<uint32_t> r(L, 0);
+  for (int b = 63; b >= 0; b--) {
+    hmod_double(r.data(), ell, L);
+    if ((c >> b) & 1) {
+      // r += 1 mod ell  (r < ell, ell odd >= 3)
+      uint64_t carry = 1;
+      for (int i = 0; i < L && carry; i++) {
+        uint64_t v = (uint64_t)r[i] + carry;
+        r[i] = (uint32_t)v;
+        carry = v >> 32;
+      }
+      bool ge = true;
+      for (int i = L - 1; i >= 0; i--)
+        if (r[i] != ell[i]) { ge = r[i] > ell[i]; break; }
+      if (ge) std::fill(r.begin(), r.end(), 0u);  // r == ell
+    }
+  }
+  for (int i = 0; i < L; i++) out[i] = r[i];
+}
+
+// ------------------------------------------------------------ objects
+
+struct sld_ctx {
+  int dev = 0;
+  int L = 0;
+  int SW = 0;
+  cudaStream_t stream = nullptr;
+  ModParams mp;
+  size_t l2_bytes = 0;
+  int sms = 0;
+};
+
+struct sld_vec {
+  sld_ctx* ctx = nullptr;
+  int64_t n = 0;
+  uint32_t* buf[2] = {nullptr, nullptr};
+  int cur = 0;
+};
+
+struct sld_xblock {
+  sld_ctx* ctx = nullptr;
+  int m = 0;
+  int64_t n = 0;
+  uint32_t* x = nullptr;  // [t][j] Montgomery form, SW stride
+};
+
+struct sld_mat {
+  sld_ctx* ctx = nullptr;
+  int64_t nrows = 0, ncols = 0, total_cols = 0, nnz = 0;
+  int n_dense = 0;
+  int npass = 1;
+  int64_t stripe_cols = 0;
+  int64_t nslices = 0;
+  int64_t n_pm = 0, n_small = 0, n_full = 0, pad_entries = 0;
+  int64_t max_deg = 0;
+  size_t dev_bytes = 0;
+  // device
+  SliceInfo* slices = nullptr;  // [npass][nslices]
+  uint4* pm_idx = nullptr;
+  uint4* s_idx = nullptr;
+  int4* s_coef = nullptr;
+  int32_t* slot_row = nullptr;
+  uint32_t* full_ptr = nullptr;
+  uint32_t* full_col = nullptr;
+  uint32_t* full_val = nullptr;
+  uint32_t* dense_val = nullptr;
+  uint32_t* part = nullptr;  // slot-indexed partials (npass > 1)
+  // host-planes convenience staging
+  uint64_t* stage = nullptr;
+  size_t stage_bytes = 0;
+  sld_vec* tmp_in = nullptr;
+  sld_vec* tmp_out = nullptr;
+  // projection scratch
+  int64_t* proj_rows = nullptr;
+  int proj_cap = 0;
+  uint32_t* terms_dev = nullptr;
+  size_t terms_cap = 0;
+  // dense-X scratch
+  uint64_t* dproj_part = nullptr;
+  size_t dproj_cap = 0;
+};
+
+// -------------------------------------------------- per-L dispatch table
+
+struct LOps {
+  void (*pass)(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
+               const ModParams& mp);
+  void (*planes_to_slots)(const uint64_t*, int, int64_t, uint32_t*, cudaStream_t);
+  void (*slots_to_planes)(const uint32_t*, int64_t, int, uint64_t*, cudaStream_t);
+  void (*limbs_to_slots)(const uint32_t*, int64_t, uint32_t*, uint32_t, cudaStream_t);
+  void (*slots_to_limbs)(const uint32_t*, int64_t, uint32_t*, uint32_t, cudaStream_t);
+  void (*to_mont)(uint32_t*, int64_t, const ModParams&, cudaStream_t);
+  void (*zero_slot)(uint32_t*, cudaStream_t);
+  void (*dense_proj)(const DenseProjArgs&, const ModParams&, cudaStream_t);
+};
+
+static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+template <int L>
+struct Ops {
+  static void pass(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
+                   const ModParams& mp) {
+    const unsigned grid = blocks_for(nslices * 32, 256);
+    if (grid == 0) return;
+    if (first && last) spmv_pass<L, true, true><<<grid, 256, 0, s>>>(a, mp);
+    else if (first) spmv_pass<L, true, false><<<grid, 256, 0, s>>>(a, mp);
+    else if (last) spmv_pass<L, false, true><<<grid, 256, 0, s>>>(a, mp);
+    else spmv_pass<L, false, false><<<grid, 256, 0, s>>>(a, mp);
+  }
+  static void p2s(const uint64_t* p, int P, int64_t n, uint32_t* o, cudaStream_t s) {
+    if (n) planes_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(p, P, n, o);
+  }
+  static void s2p(const uint32_t* i, int64_t n, int P, uint64_t* p, cudaStream_t s) {
+    if (n) slots_to_planes<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, P, p);
+  }
+  static void l2s(const uint32_t* l, int64_t n, uint32_t* o, uint32_t b, cudaStream_t s) {
+    if (n) limbs_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(l, n, o, b);
+  }
+  static void s2l(const uint32_t* i, int64_t n, uint32_t* l, uint32_t b, cudaStream_t s) {
+    if (n) slots_to_limbs<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, l, b);
+  }
+  static void mont(uint32_t* x, int64_t n, const ModParams& mp, cudaStream_t s) {
+    if (n) to_montgomery<L><<<blocks_for(n, 128), 128, 0, s>>>(x, n, mp);
+  }
+  static void zero(uint32_t* slot, cudaStream_t s) { set_zero_slot<L><<<1, 32, 0, s>>>(slot); }
+  static void dproj(const DenseProjArgs& a, const ModParams& mp, cudaStream_t s) {
+    dense_project_launch<L>(a, mp, s);
+  }
+  static LOps make() { return LOps{pass, p2s, s2p, l2s, s2l, mont, zero, dproj}; }
+};
+
+template <int L>
+static void fill_ops(LOps* t) {
+  t[L] = Ops<L>::make();
+  if constexpr (L > 1) fill_ops<L - 1>(t);
+}
+
+static const LOps& ops(int L) {
+  static LOps table[MAXL + 1];
+  static bool init = false;
+  if (!init) {
+    fill_ops<MAXL>(table);
+    init = true;
+  }
+  return table[L];
+}
+
+// ------------------------------------------------------------- context
+
+extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_ctx** out) {
+  if (!out || !ell_limbs) return fail(SLD_E_ARG, "null argument");
+  while (L > 1 && ell_limbs[L - 1] == 0) L--;
+  if (L < 1 || L > MAXL) return fail(SLD_E_ARG, "modulus must have 1..%d 32-bit words", MAXL);
+  const int bits = bitlen(ell_limbs, L);
+  if (bits < 2 || (ell_limbs[0] & 1) == 0 || (L == 1 && ell_limbs[0] < 3))
+    return fail(SLD_E_ARG, "modulus must be an odd prime >= 3");
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(SLD_E_ARG, "device %d out of range (%d)", device, ndev);
+  CU(cudaSetDevice(device));
+  auto c = std::make_unique<sld_ctx>();
+  c->dev = device;
+  c->L = L;
+  c->SW = stride_words(L);
+  ModParams& mp = c->mp;
+  memset(&mp, 0, sizeof(mp));
+  mp.L = L;
+  mp.bits = bits;
+  for (int i = 0; i < L; i++) mp.ell[i] = ell_limbs[i];
+  // K = ell * 2^48 over L+2 words: word i = (ell_{i-1} << 16) | (ell_{i-2} >> 16)
+  for (int i = 0; i < L + 2; i++) {
+    const uint32_t w1 = (i >= 1 && i - 1 < L) ? mp.ell[i - 1] : 0u;
+    const uint32_t w2 = (i >= 2 && i - 2 < L) ? mp.ell[i - 2] : 0u;
+    mp.K[i] = (w1 << 16) | (w2 >> 16);
+  }
+  // mu = floor(2^(bits-1+64) / ell): long division of 2^(bits-1) * 2^64
+  {
+    std::vector<uint32_t> r(L + 1, 0);
+    const int b = bits - 1;
+    r[b >> 5] = 1u << (b & 31);  // 2^(bits-1) < ell
+    uint64_t q = 0;
+    for (int k = 0; k < 64; k++) {
+      // r = 2r; if r >= ell: r -= ell, bit = 1
+      uint32_t c = 0;
+      for (int i = 0; i <= L; i++) {
+        uint32_t nc = r[i] >> 31;
+        r[i] = (r[i] << 1) | c;
+        c = nc;
+      }
+      bool ge = r[L] != 0;
+      if (!ge) {
+        ge = true;
+        for (int i = L - 1; i >= 0; i--)
+          if (r[i] != mp.ell[i]) { ge = r[i] > mp.ell[i]; break; }
+      }
+      q <<= 1;
+      if (ge) {
+        int64_t br = 0;
+        for (int i = 0; i <= L; i++) {
+          int64_t v = (int64_t)r[i] - (i < L ? mp.ell[i] : 0) + br;
+          r[i] = (uint32_t)v;
+          br = v >> 32;
+        }
+        q |= 1;
+      }
+    }
+    mp.mu = q;
+  }
+  // Montgomery: nprime = -ell^-1 mod 2^32, R2 = 2^(64 L) mod ell
+  {
+    uint32_t inv = 1;
+    for (int i = 0; i < 6; i++) inv *= 2u - mp.ell[0] * inv;
+    mp.nprime = 0u - inv;
+    std::vector<uint32_t> r(L, 0);
+    r[0] = 1;  // 1 < ell
+    for (int k = 0; k < 64 * L; k++) hmod_double(r.data(), mp.ell, L);
+    for (int i = 0; i < L; i++) mp.R2[i] = r[i];
+  }
+  cudaDeviceProp pr;
+  CU(cudaGetDeviceProperties(&pr, device));
+  c->l2_bytes = pr.l2CacheSize;
+  c->sms = pr.multiProcessorCount;
+  CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  *out = c.release();
+  return SLD_OK;
+}
+
+extern "C" int sld_ctx_destroy(sld_ctx* c) {
+  if (!c) return SLD_OK;
+  cudaSetDevice(c->dev);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return SLD_OK;
+}
+
+extern "C" int sld_ctx_sync(sld_ctx* c) {
+  CU(cudaSetDevice(c->dev));
+  CU(cudaStreamSynchronize(c->stream));
+  return SLD_OK;
+}
+
+// ------------------------------------------------------------- vectors
+
+static int vec_alloc_buf(sld_vec* v, int which) {
+  if (v->buf[which]) return SLD_OK;
+  const size_t words = (size_t)(v->n + 1) * v->ctx->SW;
+  CU(cudaMalloc(&v->buf[which], words * 4));
+  CU(cudaMemsetAsync(v->buf[which], 0, words * 4, v->ctx->stream));
+  ops(v->ctx->L).zero_slot(v->buf[which] + (size_t)v->n * v->ctx->SW, v->ctx->stream);
+  CU(cudaGetLastError());
+  return SLD_OK;
+}
+
+extern "C" int sld_vec_create(sld_ctx* ctx, int64_t n, sld_vec** out) {
+  if (!ctx || !out || n < 0) return fail(SLD_E_ARG, "bad vector arguments");
+  CU(cudaSetDevice(ctx->dev));
+  auto v = std::make_unique<sld_vec>();
+  v->ctx = ctx;
+  v->n = n;
+  TRY(vec_alloc_buf(v.get(), 0));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *out = v.release();
+  return SLD_OK;
+}
+
+extern "C" int sld_vec_destroy(sld_vec* v) {
+  if (!v) return SLD_OK;
+  cudaSetDevice(v->ctx->dev);
+  for (auto* b : v->buf)
+    if (b) cudaFree(b);
+  delete v;
+  return SLD_OK;
+}
+
+extern "C" int sld_vec_device_ptr(sld_vec* v, uint64_t* ptr, int64_t* stride) {
+  *ptr = (uint64_t)(uintptr_t)v->buf[v->cur];
+  *stride = v->ctx->SW;
+  return SLD_OK;
+}
+
+static int upload_planes_dev(sld_vec* v, const uint64_t* planes, int64_t n, int P, uint64_t** stage,
+                             size_t* stage_bytes) {
+  sld_ctx* c = v->ctx;
+  const size_t bytes = (size_t)n * P * 8;
+  if (*stage_bytes < bytes) {
+    if (*stage) cudaFree(*stage);
+    *stage = nullptr;
+    *stage_bytes = 0;
+    CU(cudaMalloc(stage, bytes ? bytes : 8));
+    *stage_bytes = bytes;
+  }
+  if (bytes) CU(cudaMemcpyAsync(*stage, planes, bytes, cudaMemcpyHostToDevice, c->stream));
+  ops(c->L).planes_to_slots(*stage, P, n, v->buf[v->cur], c->stream);
+  CU(cudaGetLastError());
+  return SLD_OK;
+}
+
+static int download_planes_dev(sld_vec* v, uint64_t* planes, int64_t n, int P, uint64_t** stage,
+                               size_t* stage_bytes) {
+  sld_ctx* c = v->ctx;
+  const size_t bytes = (size_t)n * P * 8;
+  if (*stage_bytes < bytes) {
+    if (*stage) cudaFree(*stage);
+    *stage = nullptr;
+    *stage_bytes = 0;
+    CU(cudaMalloc(stage, bytes ? bytes : 8));
+    *stage_bytes = bytes;
+  }
+  ops(c->L).slots_to_planes(v->buf[v->cur], n, P, *stage, c->stream);
+  CU(cudaGetLastError());
+  if (bytes) CU(cudaMemcpyAsync(planes, *stage, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return SLD_OK;
+}
+
+static int check_P(const sld_ctx* c, int P) {
+  if (P < (c->mp.bits + 15) / 16 || P > 2 * c->L + 8)
+    return fail(SLD_E_ARG, "digit-plane width %d does not fit a %d-bit modulus", P, c->mp.bits);
+  return SLD_OK;
+}
+
+extern "C" int sld_vec_upload_planes(sld_vec* v, const uint64_t* planes, int64_t n, int P) {
+  if (!v || n != v->n) return fail(SLD_E_ARG, "plane count mismatch");
+  TRY(check_P(v->ctx, P));
+  CU(cudaSetDevice(v->ctx->dev));
+  uint64_t* stage = nullptr;
+  size_t sb = 0;
+  int r = upload_planes_dev(v, planes, n, P, &stage, &sb);
+  cudaStreamSynchronize(v->ctx->stream);
+  if (stage) cudaFree(stage);
+  return r;
+}
+
+extern "C" int sld_vec_download_planes(sld_vec* v, uint64_t* planes, int64_t n, int P) {
+  if (!v || n > v->n || n < 0) return fail(SLD_E_ARG, "plane count mismatch");
+  TRY(check_P(v->ctx, P));
+  CU(cudaSetDevice(v->ctx->dev));
+  uint64_t* stage = nullptr;
+  size_t sb = 0;
+  int r = download_planes_dev(v, planes, n, P, &stage, &sb);
+  if (stage) cudaFree(stage);
+  return r;
+}
+
+extern "C" int sld_vec_upload_limbs(sld_vec* v, const uint32_t* limbs, int64_t n) {
+  if (!v || n != v->n) return fail(SLD_E_ARG, "limb count mismatch");
+  sld_ctx* c = v->ctx;
+  CU(cudaSetDevice(c->dev));
+  uint32_t* d = nullptr;
+  const size_t bytes = (size_t)n * c->L * 4;
+  CU(cudaMalloc(&d, bytes ? bytes : 4));
+  if (bytes) CU(cudaMemcpyAsync(d, limbs, bytes, cudaMemcpyHostToDevice, c->stream));
+  ops(c->L).limbs_to_slots(d, n, v->buf[v->cur], 0x80000000u, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(SLD_E_CUDA, "upload: %s", cudaGetErrorString(e));
+  return SLD_OK;
+}
+
+extern "C" int sld_vec_download_limbs(sld_vec* v, uint32_t* limbs, int64_t n) {
+  if (!v || n > v->n || n < 0) return fail(SLD_E_ARG, "limb count mismatch");
+  sld_ctx* c = v->ctx;
+  CU(cudaSetDevice(c->dev));
+  uint32_t* d = nullptr;
+  const size_t bytes = (size_t)n * c->L * 4;
+  CU(cudaMalloc(&d, bytes ? bytes : 4));
+  ops(c->L).slots_to_limbs(v->buf[v->cur], n, d, 0x80000000u, c->stream);
+  if (bytes) CU(cudaMemcpyAsync(limbs, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(SLD_E_CUDA, "download: %s", cudaGetErrorString(e));
+  return SLD_OK;
+}
+
+// -------------------------------------------------------- matrix build
+
+namespace {
+
+struct RowCounts {
+  std::vector<uint32_t> pm;  // [pass][row]
+  std::vector<uint32_t> sm;  // [pass][row]
+};
+
+template <typename F>
+void parallel_for(int64_t n, F f, int nthreads = 0) {
+  if (nthreads <= 0) nthreads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < 4096 || nthreads == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t chunk = (n + nthreads - 1) / nthreads;
+  for (int t = 0; t < nthreads; t++) {
+    const int64_t lo = t * chunk, hi = std::min<int64_t>(n, lo + chunk);
+    if (lo >= hi) break;
+    th.emplace_back([=] { f(lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
+
+template <typename T>
+int dev_upload(T** dst, const std::vector<T>& src, size_t* acct) {
+  const size_t bytes = std::max<size_t>(src.size() * sizeof(T), 16);
+  CU(cudaMalloc(dst, bytes));
+  if (!src.empty()) CU(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *acct += bytes;
+  return SLD_OK;
+}
+
+}  // namespace
+
+static void mat_free(sld_mat* m) {
+  if (!m) return;
+  void* ptrs[] = {m->slices, m->pm_idx, m->s_idx, m->s_coef, m->slot_row, m->full_ptr,
+                  m->full_col, m->full_val, m->dense_val, m->part, m->stage, m->proj_rows,
+                  m->terms_dev, m->dproj_part};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (m->tmp_in) sld_vec_destroy(m->tmp_in);
+  if (m->tmp_out) sld_vec_destroy(m->tmp_out);
+  delete m;
+}
+
+extern "C" int sld_mat_destroy(sld_mat* m) {
+  if (!m) return SLD_OK;
+  cudaSetDevice(m->ctx->dev);
+  mat_free(m);
+  return SLD_OK;
+}
+
+static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx, const uint8_t* tags,
+                     const int64_t* small_vals, int64_t n_full, const int64_t* full_pos,
+                     const uint32_t* full_limbs, const uint32_t* dense_limbs, int64_t max_stripe_cols) {
+  sld_ctx* c = M->ctx;
+  const int L = c->L, SW = c->SW;
+  const int64_t nrows = M->nrows, ncols = M->ncols;
+  const int64_t nnz = M->nnz;
+  const uint32_t PAD = (uint32_t)M->total_cols;  // zero slot
+  // ---- validation (spmatrix.py:93-126)
+  if (row_ptr[0] != 0) return fail(SLD_E_ARG, "row_ptr[0] must be 0");
+  for (int64_t r = 0; r < nrows; r++)
+    if (row_ptr[r + 1] < row_ptr[r]) return fail(SLD_E_ARG, "row_ptr must be monotone");
+  {
+    std::atomic<int> bad{0};
+    parallel_for(nnz, [&](int64_t lo, int64_t hi) {
+      for (int64_t p = lo; p < hi; p++)
+        if (col_idx[p] < 0 || col_idx[p] >= ncols || tags[p] > 3) { bad = 1; return; }
+    });
+    if (bad) return fail(SLD_E_ARG, "sparse column index out of range or unknown tag");
+  }
+  for (int64_t k = 0; k < n_full; k++) {
+    if (full_pos[k] < 0 || full_pos[k] >= nnz || (k && full_pos[k] <= full_pos[k - 1]))
+      return fail(SLD_E_ARG, "full positions must be sorted and in range");
+    if (tags[full_pos[k]] != 3) return fail(SLD_E_ARG, "full position without full tag");
+  }
+  // ---- stripes: keep the gathered column window L2-resident
+  int64_t stripe = max_stripe_cols;
+  if (stripe <= 0) {
+    const double budget = 0.40 * (double)c->l2_bytes;  // ~50 MB of the 126 MB L2
+    stripe = std::max<int64_t>(1, (int64_t)(budget / (SW * 4.0)));
+  }
+  if (stripe >= ncols) stripe = std::max<int64_t>(ncols, 1);
+  const int npass = (int)std::max<int64_t>(1, (ncols + stripe - 1) / stripe);
+  M->npass = npass;
+  M->stripe_cols = stripe;
+  // ---- per-row, per-pass class counts
+  RowCounts rc;
+  rc.pm.assign((size_t)npass * nrows, 0);
+  rc.sm.assign((size_t)npass * nrows, 0);
+  std::vector<uint32_t> fcount(nrows + 1, 0);
+  // map flat position -> full value index (only for tag 3); sorted positions
+  std::atomic<int> bound_bad{0};
+  parallel_for(nrows, [&](int64_t lo, int64_t hi) {
+    for (int64_t r = lo; r < hi; r++) {
+      uint32_t tot_s = 0, tot_pm = 0, nf = 0;
+      for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; p++) {
+        const int t = tags[p];
+        const int pass = (int)(col_idx[p] / stripe);
+        if (t <= 1) {
+          rc.pm[(size_t)pass * nrows + r]++;
+          tot_pm++;
+        } else if (t == 2) {
+          const int64_t v = small_vals[p];
+          if (v > -0x80000000ll && v < 0x80000000ll) {
+            rc.sm[(size_t)pass * nrows + r]++;
+            tot_s++;
+          } else {
+            nf++;
+          }
+        } else {
+          nf++;
+        }
+      }
+      fcount[r] = nf;
+      if (tot_s > (1u << 15) || tot_pm > (1u << 24)) bound_bad = 1;
+    }
+  });
+  if (bound_bad)
+    return fail(SLD_E_BOUND, "row degree too large for exact accumulation "
+                             "(> 2^15 small or > 2^24 +-1 entries in a row)");
+  // ---- slot order: rows sorted by (+-1 count, small count) descending
+  std::vector<int64_t> tot_pm(nrows, 0), tot_s(nrows, 0);
+  parallel_for(nrows, [&](int64_t lo, int64_t hi) {
+    for (int64_t r = lo; r < hi; r++) {
+      int64_t a = 0, b = 0;
+      for (int p = 0; p < npass; p++) {
+        a += rc.pm[(size_t)p * nrows + r];
+        b += rc.sm[(size_t)p * nrows + r];
+      }
+      tot_pm[r] = a;
+      tot_s[r] = b;
+    }
+  });
+  std::vector<int32_t> order(nrows);
+  for (int64_t r = 0; r < nrows; r++) order[r] = (int32_t)r;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+    if (tot_pm[x] != tot_pm[y]) return tot_pm[x] > tot_pm[y];
+    return tot_s[x] > tot_s[y];
+  });
+  const int64_t nslices = (nrows + 31) / 32;
+  M->nslices = nslices;
+  const int64_t nslots = nslices * 32;
+  std::vector<int32_t> slot_row(nslots, -1);
+  for (int64_t s = 0; s < nrows; s++) slot_row[s] = order[s];
+  // ---- slice tables
+  std::vector<SliceInfo> slices((size_t)npass * nslices);
+  uint64_t pm_units = 0, s_units = 0;
+  for (int p = 0; p < npass; p++) {
+    for (int64_t s = 0; s < nslices; s++) {
+      uint32_t kpm = 0, ks = 0;
+      for (int l = 0; l < 32; l++) {
+        const int32_t r = slot_row[s * 32 + l];
+        if (r < 0) continue;
+        kpm = std::max(kpm, (rc.pm[(size_t)p * nrows + r] + 3) / 4);
+        ks = std::max(ks, (rc.sm[(size_t)p * nrows + r] + 3) / 4);
+      }
+      SliceInfo& si = slices[(size_t)p * nslices + s];
+      si.pm_off = (uint32_t)pm_units;
+      si.pm_k4 = kpm;
+      si.s_off = (uint32_t)s_units;
+      si.s_k4 = ks;
+      pm_units += (uint64_t)kpm * 32;
+      s_units += (uint64_t)ks * 32;
+      if (pm_units >= (1ull << 32) || s_units >= (1ull << 32))
+        return fail(SLD_E_BOUND, "matrix too large for 32-bit slice offsets");
+    }
+  }
+  // ---- entry streams
+  std::vector<uint32_t> pm_idx(pm_units * 4, PAD);
+  std::vector<uint32_t> s_idx(s_units * 4, PAD);
+  std::vector<int32_t> s_coef(s_units * 4, 0);
+  // full entries CSR over slots
+  std::vector<uint32_t> full_ptr(nslots + 1, 0);
+  for (int64_t s = 0; s < nslots; s++) {
+    const int32_t r = slot_row[s];
+    full_ptr[s + 1] = full_ptr[s] + (r >= 0 ? fcount[r] : 0);
+  }
+  const int64_t nf_total = full_ptr[nslots];
+  std::vector<uint32_t> full_col(nf_total);
+  std::vector<uint32_t> full_val((size_t)nf_total * SW, 0);
+  std::atomic<int64_t> pads{0};
+  parallel_for(nslots, [&](int64_t lo, int64_t hi) {
+    std::vector<uint32_t> kp(npass), ks(npass);
+    int64_t mypads = 0;
+    for (int64_t slot = lo; slot < hi; slot++) {
+      const int32_t r = slot_row[slot];
+      if (r < 0) continue;
+      const int64_t slice = slot >> 5;
+      const int lane = (int)(slot & 31);
+      std::fill(kp.begin(), kp.end(), 0u);
+      std::fill(ks.begin(), ks.end(), 0u);
+      uint32_t fk = full_ptr[slot];
+      for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; p++) {
+        const int t = tags[p];
+        const uint32_t col = (uint32_t)col_idx[p];
+        const int pass = (int)(col_idx[p] / stripe);
+        const SliceInfo& si = slices[(size_t)pass * nslices + slice];
+        if (t <= 1) {
+          const uint32_t k = kp[pass]++;
+          const uint64_t pos = ((uint64_t)si.pm_off + (uint64_t)(k >> 2) * 32 + lane) * 4 + (k & 3);
+          pm_idx[pos] = col | (t == 1 ? 0x80000000u : 0u);
+          continue;
+        }
+        if (t == 2) {
+          const int64_t v = small_vals[p];
+          if (v > -0x80000000ll && v < 0x80000000ll) {
+            const uint32_t k = ks[pass]++;
+            const uint64_t pos = ((uint64_t)si.s_off + (uint64_t)(k >> 2) * 32 + lane) * 4 + (k & 3);
+            s_idx[pos] = col;
+            s_coef[pos] = (int32_t)v;
+            continue;
+          }
+          // promoted: value = v mod ell
+          uint32_t* dst = &full_val[(size_t)fk * SW];
+          hmod_u64(v < 0 ? (uint64_t)(-(v + 1)) + 1 : (uint64_t)v, c->mp.ell, L, dst);
+          bool nz = false;
+          for (int i = 0; i < L; i++) nz |= dst[i] != 0;
+          if (v < 0 && nz) {  // ell - (|v| mod ell)
+            int64_t br = 0;
+            for (int i = 0; i < L; i++) {
+              int64_t x = (int64_t)c->mp.ell[i] - dst[i] + br;
+              dst[i] = (uint32_t)x;
+              br = x >> 32;
+            }
+          }
+          full_col[fk++] = col;
+          continue;
+        }
+        // tag 3: locate value by binary search over sorted full_pos
+        const int64_t* it = std::lower_bound(full_pos, full_pos + n_full, p);
+        const int64_t fi = it - full_pos;
+        uint32_t* dst = &full_val[(size_t)fk * SW];
+        if (fi < n_full && *it == p)
+          for (int i = 0; i < L; i++) dst[i] = full_limbs[(size_t)fi * L + i];
+        full_col[fk++] = col;
+      }
+      for (int q = 0; q < npass; q++) {
+        const SliceInfo& si = slices[(size_t)q * nslices + slice];
+        mypads += (int64_t)si.pm_k4 * 4 - kp[q] + (int64_t)si.s_k4 * 4 - ks[q];
+      }
+    }
+    pads += mypads;
+  });
+  // every tag-3 position must have had a value
+  {
+    int64_t n3 = 0;
+    for (int64_t p = 0; p < nnz; p++) n3 += tags[p] == 3;
+    if (n3 != n_full) return fail(SLD_E_ARG, "%lld full-tag entries but %lld full values",
+                                  (long long)n3, (long long)n_full);
+  }
+  // ---- dense columns [g][slot-padded row]
+  std::vector<uint32_t> dense_val;
+  if (M->n_dense) {
+    dense_val.assign((size_t)M->n_dense * nslots * SW, 0);
+    for (int g = 0; g < M->n_dense; g++)
+      for (int64_t r = 0; r < nrows; r++)
+        for (int i = 0; i < L; i++)
+          dense_val[((size_t)g * nslots + r) * SW + i] = dense_limbs[((size_t)g * nrows + r) * L + i];
+  }
+  // ---- stats
+  int64_t npm = 0, nsm = 0, mdeg = 0;
+  for (int64_t r = 0; r < nrows; r++) {
+    npm += tot_pm[r];
+    nsm += tot_s[r];
+    mdeg = std::max<int64_t>(mdeg, row_ptr[r + 1] - row_ptr[r] + M->n_dense);
+  }
+  M->n_pm = npm;
+  M->n_small = nsm;
+  M->n_full = nf_total + (int64_t)M->n_dense * nrows;
+  M->pad_entries = pads;
+  M->max_deg = mdeg;
+  // ---- upload
+  CU(cudaSetDevice(c->dev));
+  size_t acct = 0;
+  TRY(dev_upload(&M->slices, slices, &acct));
+  CU(cudaMalloc(&M->pm_idx, std::max<size_t>(pm_idx.size() * 4, 16)));
+  if (!pm_idx.empty()) CU(cudaMemcpy(M->pm_idx, pm_idx.data(), pm_idx.size() * 4, cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&M->s_idx, std::max<size_t>(s_idx.size() * 4, 16)));
+  if (!s_idx.empty()) CU(cudaMemcpy(M->s_idx, s_idx.data(), s_idx.size() * 4, cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&M->s_coef, std::max<size_t>(s_coef.size() * 4, 16)));
+  if (!s_coef.empty()) CU(cudaMemcpy(M->s_coef, s_coef.data(), s_coef.size() * 4, cudaMemcpyHostToDevice));
+  acct += pm_idx.size() * 4 + s_idx.size() * 4 + s_coef.size() * 4;
+  TRY(dev_upload(&M->slot_row, slot_row, &acct));
+  TRY(dev_upload(&M->full_ptr, full_ptr, &acct));
+  TRY(dev_upload(&M->full_col, full_col, &acct));
+  TRY(dev_upload(&M->full_val, full_val, &acct));
+  if (nf_total) ops(L).to_mont(M->full_val, nf_total, c->mp, c->stream);
+  if (M->n_dense) {
+    TRY(dev_upload(&M->dense_val, dense_val, &acct));
+    ops(L).to_mont(M->dense_val, (int64_t)M->n_dense * nslots, c->mp, c->stream);
+  }
+  if (npass > 1) {
+    CU(cudaMalloc(&M->part, (size_t)nslots * SW * 4));
+    acct += (size_t)nslots * SW * 4;
+  }
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(c->stream));
+  M->dev_bytes = acct;
+  return SLD_OK;
+}
+
+extern "C" int sld_mat_create(sld_ctx* ctx, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                              const int32_t* col_idx, const uint8_t* tags, const int64_t* small_vals,
+                              int64_t n_full, const int64_t* full_pos, const uint32_t* full_limbs,
+                              int n_dense, const uint32_t* dense_limbs, int64_t max_stripe_cols,
+                              sld_mat** out) {
+  if (!ctx || !out || !row_ptr || nrows < 0 || ncols < 0 || n_dense < 0 || n_full < 0)
+    return fail(SLD_E_ARG, "bad matrix arguments");
+  if (nrows >= 0x7FFFFFFF || ncols + n_dense >= 0x7FFFFFFF)
+    return fail(SLD_E_ARG, "dimensions must be < 2^31");
+  const int64_t nnz = row_ptr[nrows];
+  if (nnz && (!col_idx || !tags || !small_vals)) return fail(SLD_E_ARG, "null entry arrays");
+  if (n_dense && !dense_limbs) return fail(SLD_E_ARG, "null dense column values");
+  if (n_full && (!full_pos || !full_limbs)) return fail(SLD_E_ARG, "null full entries");
+  CU(cudaSetDevice(ctx->dev));
+  sld_mat* M = new sld_mat();
+  M->ctx = ctx;
+  M->nrows = nrows;
+  M->ncols = ncols;
+  M->n_dense = n_dense;
+  M->total_cols = ncols + n_dense;
+  M->nnz = nnz;
+  int r = mat_build(M, row_ptr, col_idx, tags, small_vals, n_full, full_pos, full_limbs, dense_limbs,
+                    max_stripe_cols);
+  if (r != SLD_OK) {
+    mat_free(M);
+    return r;
+  }
+  *out = M;
+  return SLD_OK;
+}
+
+extern "C" int sld_mat_info(const sld_mat* m, int64_t* info) {
+  if (!m || !info) return fail(SLD_E_ARG, "null argument");
+  int64_t v[16] = {m->nrows, m->total_cols, m->nnz, m->n_pm, m->n_small, m->n_full,
+                   m->npass, m->nslices, (int64_t)m->dev_bytes, m->pad_entries,
+                   m->ctx->L, m->ctx->SW, m->max_deg, m->stripe_cols, 0, 0};
+  memcpy(info, v, sizeof(v));
+  return SLD_OK;
+}
+
+// ------------------------------------------------------------- SpMV
+
+// launch all stripe passes of one product on the context stream
+static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows,
+                           int proj_m, uint32_t* terms_out) {
+  sld_ctx* c = M->ctx;
+  SpmvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.x = x;
+  a.y = y;
+  a.part_in = M->part;
+  a.part_out = M->part;
+  a.pm_idx = M->pm_idx;
+  a.s_idx = M->s_idx;
+  a.s_coef = M->s_coef;
+  a.slot_row = M->slot_row;
+  a.full_ptr = M->full_ptr;
+  a.full_col = M->full_col;
+  a.full_val = M->full_val;
+  a.dense_val = M->dense_val;
+  a.n_dense = M->n_dense;
+  a.dense_col0 = M->ncols;
+  a.proj_rows = proj_rows;
+  a.proj_m = proj_m;
+  a.terms_out = terms_out;
+  a.nslices = M->nslices;
+  a.has_full = (M->full_ptr && M->n_full) ? 1 : 0;
+  const LOps& o = ops(c->L);
+  if (M->nslices == 0) {
+    // no rows: still record the projection
+    if (proj_m) {
+      a.nslices = 0;
+      a.slices = M->slices;
+      o.pass(1, 1, 1, c->stream, a, c->mp);
+    }
+    return;
+  }
+  for (int p = 0; p < M->npass; p++) {
+    a.slices = M->slices + (size_t)p * M->nslices;
+    o.pass(p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
+  }
+}
+
+extern "C" int sld_spmv(sld_mat* M, sld_vec* in, sld_vec* out) {
+  if (!M || !in || !out) return fail(SLD_E_ARG, "null argument");
+  if (in->n != M->total_cols) return fail(SLD_E_ARG, "vector length %lld != %lld columns",
+                                          (long long)in->n, (long long)M->total_cols);
+  if (out->n < M->nrows) return fail(SLD_E_ARG, "output vector too short");
+  if (in == out) return fail(SLD_E_ARG, "in and out must differ");
+  if (in->ctx != M->ctx || out->ctx != M->ctx) return fail(SLD_E_ARG, "context mismatch");
+  CU(cudaSetDevice(M->ctx->dev));
+  launch_product(M, in->buf[in->cur], out->buf[out->cur], nullptr, 0, nullptr);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(M->ctx->stream));
+  return SLD_OK;
+}
+
+extern "C" int sld_spmv_planes(sld_mat* M, const uint64_t* in_planes, uint64_t* out_planes, int P) {
+  if (!M) return fail(SLD_E_ARG, "null matrix");
+  sld_ctx* c = M->ctx;
+  TRY(check_P(c, P));
+  CU(cudaSetDevice(c->dev));
+  if (!M->tmp_in) TRY(sld_vec_create(c, M->total_cols, &M->tmp_in));
+  if (!M->tmp_out) TRY(sld_vec_create(c, M->nrows, &M->tmp_out));
+  TRY(upload_planes_dev(M->tmp_in, in_planes, M->total_cols, P, &M->stage, &M->stage_bytes));
+  launch_product(M, M->tmp_in->buf[0], M->tmp_out->buf[0], nullptr, 0, nullptr);
+  CU(cudaGetLastError());
+  TRY(download_planes_dev(M->tmp_out, out_planes, M->nrows, P, &M->stage, &M->stage_bytes));
+  return SLD_OK;
+}
+
+// ------------------------------------------------------------- Krylov
+
+static int ensure_proj(sld_mat* M, const int64_t* x_rows, int m, int64_t chunk) {
+  sld_ctx* c = M->ctx;
+  if (m > 256) return fail(SLD_E_ARG, "at most 256 unit projection rows");
+  for (int t = 0; t < m; t++)
+    if (x_rows[t] < 0 || x_rows[t] >= M->total_cols) return fail(SLD_E_ARG, "projection row out of range");
+  if (M->proj_cap < m) {
+    if (M->proj_rows) cudaFree(M->proj_rows);
+    M->proj_rows = nullptr;
+    CU(cudaMalloc(&M->proj_rows, std::max(m, 1) * 8));
+    M->proj_cap = m;
+  }
+  if (m) CU(cudaMemcpyAsync(M->proj_rows, x_rows, m * 8, cudaMemcpyHostToDevice, c->stream));
+  const size_t need = (size_t)std::max<int64_t>(chunk, 1) * std::max(m, 1) * c->SW;
+  if (M->terms_cap < need) {
+    if (M->terms_dev) cudaFree(M->terms_dev);
+    M->terms_dev = nullptr;
+    CU(cudaMalloc(&M->terms_dev, need * 4));
+    M->terms_cap = need;
+  }
+  return SLD_OK;
+}
+
+// copy `steps` terms from device (SW stride, at `src`) into host limbs
+static int drain_terms(sld_mat* M, const uint32_t* src, int m, int64_t steps, uint32_t* host,
+                       std::vector<uint32_t>& tmp) {
+  sld_ctx* c = M->ctx;
+  const size_t words = (size_t)steps * m * c->SW;
+  if (!words) {
+    CU(cudaStreamSynchronize(c->stream));
+    return SLD_OK;
+  }
+  tmp.resize(words);
+  CU(cudaMemcpyAsync(tmp.data(), src, words * 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  const int L = c->L, SW = c->SW;
+  for (int64_t k = 0; k < steps * m; k++)
+    for (int i = 0; i < L; i++) host[k * L + i] = tmp[k * SW + i];
+  return SLD_OK;
+}
+
+static constexpr int64_t KRYLOV_CHUNK = 1024;  // steps between host drains of the terms
+static constexpr int GRAPH_STEPS = 32;          // products captured in one CUDA graph (even)
+
+extern "C" int sld_krylov_unit(sld_mat* M, sld_vec* v, const int64_t* x_rows, int m, int64_t steps,
+                               uint32_t* terms) {
+  if (!M || !v || steps < 0 || m < 0) return fail(SLD_E_ARG, "bad Krylov arguments");
+  if (M->nrows != M->total_cols) return fail(SLD_E_ARG, "Krylov needs a square matrix");
+  if (v->n != M->total_cols) return fail(SLD_E_ARG, "iterate length mismatch");
+  if (v->ctx != M->ctx) return fail(SLD_E_ARG, "context mismatch");
+  if (m && (!x_rows || !terms)) return fail(SLD_E_ARG, "null projection arrays");
+  sld_ctx* c = M->ctx;
+  CU(cudaSetDevice(c->dev));
+  TRY(vec_alloc_buf(v, v->cur ^ 1));
+  // terms_dev: [0, GRAPH_STEPS) graph scratch, then the chunk accumulation area
+  TRY(ensure_proj(M, x_rows, m, GRAPH_STEPS + KRYLOV_CHUNK));
+  const size_t tstride = (size_t)m * c->SW;  // words per step
+  uint32_t* scratch = M->terms_dev;
+  uint32_t* area = M->terms_dev + (size_t)GRAPH_STEPS * tstride;
+  std::vector<uint32_t> tmp;
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // graphs starting from buffer 0 / 1
+  auto capture = [&](int start) -> int {
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int cur = start;
+    for (int k = 0; k < GRAPH_STEPS; k++) {
+      launch_product(M, v->buf[cur], v->buf[cur ^ 1], M->proj_rows, m, scratch + k * tstride);
+      cur ^= 1;
+    }
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (e != cudaSuccess) return fail(SLD_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    CU(cudaGraphInstantiate(&exec[start], g, 0));
+    CU(cudaGraphDestroy(g));
+    return SLD_OK;
+  };
+  int rc = SLD_OK;
+  int64_t done = 0;
+  while (done < steps && rc == SLD_OK) {
+    const int64_t chunk = std::min<int64_t>(KRYLOV_CHUNK, steps - done);
+    int64_t k = 0;
+    while (k + GRAPH_STEPS <= chunk) {
+      if (!exec[v->cur] && (rc = capture(v->cur)) != SLD_OK) break;
+      cudaError_t e = cudaGraphLaunch(exec[v->cur], c->stream);
+      if (e == cudaSuccess && m)
+        e = cudaMemcpyAsync(area + k * tstride, scratch, GRAPH_STEPS * tstride * 4,
+                            cudaMemcpyDeviceToDevice, c->stream);
+      if (e != cudaSuccess) { rc = fail(SLD_E_CUDA, "graph replay: %s", cudaGetErrorString(e)); break; }
+      k += GRAPH_STEPS;  // GRAPH_STEPS is even: the iterate is back in the same buffer
+    }
+    if (rc) break;
+    for (; k < chunk; k++) {
+      launch_product(M, v->buf[v->cur], v->buf[v->cur ^ 1], M->proj_rows, m, area + k * tstride);
+      v->cur ^= 1;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { rc = fail(SLD_E_CUDA, "launch: %s", cudaGetErrorString(e)); break; }
+    rc = drain_terms(M, area, m, chunk, m ? terms + (size_t)done * m * c->L : nullptr, tmp);
+    done += chunk;
+  }
+  for (auto& x : exec)
+    if (x) cudaGraphExecDestroy(x);
+  return rc;
+}
+
+// ------------------------------------------------------------- dense X
+
+extern "C" int sld_xblock_create(sld_ctx* ctx, const uint32_t* x_limbs, int m, int64_t n,
+                                 sld_xblock** out) {
+  if (!ctx || !out || m < 0 || n < 0 || (m && n && !x_limbs)) return fail(SLD_E_ARG, "bad x block");
+  CU(cudaSetDevice(ctx->dev));
+  auto xb = std::make_unique<sld_xblock>();
+  xb->ctx = ctx;
+  xb->m = m;
+  xb->n = n;
+  const size_t cnt = (size_t)m * n;
+  CU(cudaMalloc(&xb->x, std::max<size_t>(cnt * ctx->SW * 4, 16)));
+  if (cnt) {
+    uint32_t* d = nullptr;
+    CU(cudaMalloc(&d, cnt * ctx->L * 4));
+    CU(cudaMemcpyAsync(d, x_limbs, cnt * ctx->L * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ops(ctx->L).limbs_to_slots(d, (int64_t)cnt, xb->x, 0u, ctx->stream);
+    ops(ctx->L).to_mont(xb->x, (int64_t)cnt, ctx->mp, ctx->stream);
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(SLD_E_CUDA, "x block upload: %s", cudaGetErrorString(e));
+  }
+  *out = xb.release();
+  return SLD_OK;
+}
+
+extern "C" int sld_xblock_destroy(sld_xblock* x) {
+  if (!x) return SLD_OK;
+  cudaSetDevice(x->ctx->dev);
+  if (x->x) cudaFree(x->x);
+  delete x;
+  return SLD_OK;
+}
+
+extern "C" int sld_krylov_dense(sld_mat* M, sld_vec* v, sld_xblock* X, int64_t steps, uint32_t* terms) {
+  if (!M || !v || !X || steps < 0) return fail(SLD_E_ARG, "bad Krylov arguments");
+  if (M->nrows != M->total_cols) return fail(SLD_E_ARG, "Krylov needs a square matrix");
+  if (v->n != M->total_cols || X->n != M->total_cols) return fail(SLD_E_ARG, "length mismatch");
+  sld_ctx* c = M->ctx;
+  CU(cudaSetDevice(c->dev));
+  TRY(vec_alloc_buf(v, v->cur ^ 1));
+  const int m = X->m;
+  TRY(ensure_proj(M, nullptr, 0, KRYLOV_CHUNK));
+  {
+    const size_t need = (size_t)KRYLOV_CHUNK * std::max(m, 1) * c->SW;
+    if (M->terms_cap < need) {
+      if (M->terms_dev) cudaFree(M->terms_dev);
+      M->terms_dev = nullptr;
+      CU(cudaMalloc(&M->terms_dev, need * 4));
+      M->terms_cap = need;
+    }
+  }
+  DenseProjArgs da;
+  if (dense_proj_prepare(M->ctx->sms, m, v->n, c->SW, &M->dproj_part, &M->dproj_cap, &da))
+    return fail(SLD_E_CUDA, "dense projection scratch allocation failed");
+  da.x = X->x;
+  std::vector<uint32_t> tmp;
+  int64_t done = 0;
+  while (done < steps) {
+    const int64_t chunk = std::min<int64_t>(KRYLOV_CHUNK, steps - done);
+    for (int64_t k = 0; k < chunk; k++) {
+      da.v = v->buf[v->cur];
+      da.out = M->terms_dev + (size_t)k * m * c->SW;
+      if (m) ops(c->L).dense_proj(da, c->mp, c->stream);
+      launch_product(M, v->buf[v->cur], v->buf[v->cur ^ 1], nullptr, 0, nullptr);
+      v->cur ^= 1;
+    }
+    CU(cudaGetLastError());
+    TRY(drain_terms(M, M->terms_dev, m, chunk, m ? terms + (size_t)done * m * c->L : nullptr, tmp));
+    done += chunk;
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return SLD_OK;
+}
+
+// ------------------------------------------------------------- bench hook
+
+extern "C" int sld_bench_spmv(sld_mat* M, sld_vec* v, int64_t steps, int warmup, double* total_ms,
+                              double* kernel_ms) {
+  if (!M || !v || steps < 1) return fail(SLD_E_ARG, "bad bench arguments");
+  if (M->nrows != M->total_cols || v->n != M->total_cols) return fail(SLD_E_ARG, "square matrix needed");
+  sld_ctx* c = M->ctx;
+  CU(cudaSetDevice(c->dev));
+  TRY(vec_alloc_buf(v, v->cur ^ 1));
+  // graph of 2 products (returns to the same buffer)
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  launch_product(M, v->buf[v->cur], v->buf[v->cur ^ 1], nullptr, 0, nullptr);
+  launch_product(M, v->buf[v->cur ^ 1], v->buf[v->cur], nullptr, 0, nullptr);
+  CU(cudaStreamEndCapture(c->stream, &g));
+  CU(cudaGraphInstantiate(&ge, g, 0));
+  CU(cudaGraphDestroy(g));
+  for (int w = 0; w < (warmup + 1) / 2; w++) CU(cudaGraphLaunch(ge, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  const int64_t pairs = (steps + 1) / 2;
+  CU(cudaEventRecord(e0, c->stream));
+  for (int64_t k = 0; k < pairs; k++) CU(cudaGraphLaunch(ge, c->stream));
+  CU(cudaEventRecord(e1, c->stream));
+  CU(cudaEventSynchronize(e1));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
+  *total_ms = ms;
+  *kernel_ms = ms / (2.0 * pairs);
+  return SLD_OK;
+}

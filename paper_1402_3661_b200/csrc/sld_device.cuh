@@ -1,0 +1,432 @@
+// sld_device.cuh -- device-side arithmetic and kernels of the B200 Krylov
+// SpMV engine (sm_100a).  See DESIGN.md for the data layout and the bounds.
+//
+// Vector layout in HBM: one residue per slot, `SW` 32-bit words per slot
+// (SW = L rounded up to 8, i.e. whole 32-byte sectors), limbs little-endian
+// and *biased*: word i holds (limb_i XOR 0x80000000), i.e. limb_i - 2^31 as a
+// signed int32.  The bias lets one signed IMAD.WIDE (s32 x s32 + s64) do the
+// multiply-accumulate of a signed coefficient with a limb; the bias is
+// removed exactly per row from the running coefficient sum S:
+//     sum_e c_e u_e = sum_i 2^(32 i) (sum_e c_e (u_ei - 2^31)) + 2^31 S sum_i 2^(32 i).
+// Slot `total_cols` of every input vector is the zero residue, the target
+// of padded index entries.
+#pragma once
+#include <cstdint>
+
+namespace sld {
+
+constexpr int MAXL = 32;  // 1024-bit moduli (the reference accepts <= 1024 bits)
+
+struct ModParams {
+  uint32_t ell[MAXL + 1];
+  uint32_t K[MAXL + 3];  // ell * 2^48 in L+2 words: makes the row value positive
+  uint32_t R2[MAXL + 1]; // 2^(64 L) mod ell (Montgomery conversion)
+  uint64_t mu;           // floor(2^(bits-1+64) / ell)  (Barrett)
+  uint32_t nprime;       // -ell^-1 mod 2^32            (Montgomery)
+  int bits;              // bit length of ell
+  int L;
+};
+
+__host__ __device__ constexpr int stride_words(int L) { return ((L + 7) / 8) * 8; }
+
+struct SliceInfo {
+  uint32_t pm_off;  // uint4 units into pm_idx
+  uint32_t pm_k4;   // groups of 4 +-1 entries per lane
+  uint32_t s_off;   // uint4 units into s_idx / s_coef
+  uint32_t s_k4;    // groups of 4 small entries per lane
+};
+
+struct SpmvArgs {
+  const uint32_t* x;        // input vector (biased), total_cols+1 slots
+  uint32_t* y;              // output vector (biased), row-indexed (last pass)
+  const uint32_t* part_in;  // slot-indexed canonical partials (pass > 0)
+  uint32_t* part_out;       // slot-indexed canonical partials (pass < last)
+  const SliceInfo* slices;  // this pass's slice table
+  const uint4* pm_idx;      // +-1 entries: col | sign<<31
+  const uint4* s_idx;       // small entries: col
+  const int4* s_coef;       // small entries: signed coefficient, |c| < 2^31
+  const int32_t* slot_row;  // output row of each slot (-1 = padding slot)
+  // full-class entries and dense columns (last pass only)
+  const uint32_t* full_ptr; // per slot, CSR into full_col/full_val
+  const uint32_t* full_col;
+  const uint32_t* full_val; // Montgomery form, SW words each
+  const uint32_t* dense_val;// [g][row] Montgomery form, SW words each
+  int n_dense;
+  int64_t dense_col0;       // global column index of dense column 0
+  // unit-X projection of the INPUT vector (first pass only)
+  const int64_t* proj_rows;
+  int proj_m;
+  uint32_t* terms_out;      // proj_m slots of SW words, canonical (unbiased)
+  int64_t nslices;
+  int has_full;
+};
+
+// ---------------------------------------------------------------- loads
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* a, uint64_t pol) {
+  static_assert(sizeof(T) == 16, "128-bit stream loads");
+  uint32_t r0, r1, r2, r3;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "l"(a), "l"(pol));
+  T v;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+  w[0] = r0; w[1] = r1; w[2] = r2; w[3] = r3;
+  return v;
+}
+
+// gather one residue slot (SW words, 32-byte sectors) through L1/L2
+template <int SW>
+__device__ __forceinline__ void gather(const uint32_t* __restrict__ p, uint32_t (&u)[SW]) {
+#pragma unroll
+  for (int q = 0; q < SW / 8; q++) {
+    asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(u[8 * q + 0]), "=r"(u[8 * q + 1]), "=r"(u[8 * q + 2]), "=r"(u[8 * q + 3]),
+          "=r"(u[8 * q + 4]), "=r"(u[8 * q + 5]), "=r"(u[8 * q + 6]), "=r"(u[8 * q + 7])
+        : "l"(p + 8 * q));
+  }
+}
+
+template <int SW>
+__device__ __forceinline__ void store_slot(uint32_t* p, const uint32_t (&u)[SW]) {
+#pragma unroll
+  for (int q = 0; q < SW / 8; q++) {
+    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p + 8 * q),
+                 "r"(u[8 * q + 0]), "r"(u[8 * q + 1]), "r"(u[8 * q + 2]), "r"(u[8 * q + 3]),
+                 "r"(u[8 * q + 4]), "r"(u[8 * q + 5]), "r"(u[8 * q + 6]), "r"(u[8 * q + 7]));
+  }
+}
+
+// ---------------------------------------------------------- arithmetic
+
+// r = a * b * 2^(-32 L) mod ell (CIOS Montgomery), a, b < ell -> r < ell
+template <int L>
+__device__ __forceinline__ void montmul(const uint32_t* a, const uint32_t* b, const ModParams& mp,
+                                        uint32_t* r) {
+  uint32_t t[L + 2];
+#pragma unroll
+  for (int j = 0; j < L + 2; j++) t[j] = 0;
+#pragma unroll 1
+  for (int i = 0; i < L; i++) {
+    uint64_t c = 0;
+    const uint32_t bi = b[i];
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+      c = (uint64_t)a[j] * bi + t[j] + (c >> 32);
+      t[j] = (uint32_t)c;
+    }
+    uint64_t s = (uint64_t)t[L] + (c >> 32);
+    t[L] = (uint32_t)s;
+    t[L + 1] = (uint32_t)(s >> 32);
+    const uint32_t m = t[0] * mp.nprime;
+    c = (uint64_t)m * mp.ell[0] + t[0];
+#pragma unroll
+    for (int j = 1; j < L; j++) {
+      c = (uint64_t)m * mp.ell[j] + t[j] + (c >> 32);
+      t[j - 1] = (uint32_t)c;
+    }
+    s = (uint64_t)t[L] + (c >> 32);
+    t[L - 1] = (uint32_t)s;
+    t[L] = t[L + 1] + (uint32_t)(s >> 32);
+  }
+  // conditional subtract
+  uint32_t d[L + 1];
+  int64_t br = 0;
+#pragma unroll
+  for (int j = 0; j <= L; j++) {
+    int64_t v = (int64_t)t[j] - (j < L ? mp.ell[j] : 0) + br;
+    d[j] = (uint32_t)v;
+    br = v >> 32;
+  }
+  const bool ge = br == 0;
+#pragma unroll
+  for (int j = 0; j < L; j++) r[j] = ge ? d[j] : t[j];
+}
+
+// Reduce the row value V = sum_i 2^(32i) (a_i + 2^16 b_i) to [0, ell).
+// a_i = acc_i + 2^31 Slo, b_i = acc2_i + 2^31 Shi; |V| < 2^47 ell by the
+// per-row count bounds enforced at build time.
+template <int L>
+__device__ __forceinline__ void finalize(const int64_t (&acc)[L], const int64_t (&acc2)[L],
+                                         int64_t Slo, int64_t Shi, const ModParams& mp,
+                                         uint32_t (&R)[L]) {
+  uint32_t w[L + 2];
+  const int64_t blo = Slo * ((int64_t)1 << 31), bhi = Shi * ((int64_t)1 << 31);
+  int64_t carry = 0, prev_hi = 0;
+#pragma unroll
+  for (int i = 0; i < L + 2; i++) {
+    int64_t t = carry + prev_hi;
+    if (i < L) {
+      const int64_t a = acc[i] + blo;
+      const int64_t b = acc2[i] + bhi;
+      t += a + ((b & 0xFFFF) << 16);
+      prev_hi = b >> 16;
+    } else {
+      prev_hi = 0;
+    }
+    w[i] = (uint32_t)t;
+    carry = t >> 32;
+  }
+  // V' = V + ell * 2^48 >= 0
+  uint64_t c = 0;
+#pragma unroll
+  for (int i = 0; i < L + 2; i++) {
+    c = (uint64_t)w[i] + mp.K[i] + (c >> 32);
+    w[i] = (uint32_t)c;
+  }
+  // t = V' >> (bits-1): the top word index is L-1 for every modulus of L words
+  const int sh = mp.bits - 1 - 32 * (L - 1);
+  const unsigned __int128 top = ((unsigned __int128)w[L + 1] << 64) |
+                                ((unsigned __int128)w[L] << 32) | w[L - 1];
+  const uint64_t tq = (uint64_t)(top >> sh);
+  const uint64_t q = __umul64hi(tq, mp.mu);  // q - 2 <= q_hat <= q
+  const uint32_t q0 = (uint32_t)q, q1 = (uint32_t)(q >> 32);
+  uint32_t P[L + 1];
+  uint64_t m = 0;
+#pragma unroll
+  for (int j = 0; j < L; j++) {
+    m = (uint64_t)q0 * mp.ell[j] + (m >> 32);
+    P[j] = (uint32_t)m;
+  }
+  P[L] = (uint32_t)(m >> 32);
+  m = 0;
+#pragma unroll
+  for (int j = 0; j < L; j++) {
+    m = (uint64_t)q1 * mp.ell[j] + P[j + 1] + (m >> 32);
+    P[j + 1] = (uint32_t)m;
+  }
+  uint32_t r[L + 1];
+  int64_t br = 0;
+#pragma unroll
+  for (int j = 0; j <= L; j++) {
+    int64_t v = (int64_t)w[j] - P[j] + br;
+    r[j] = (uint32_t)v;
+    br = v >> 32;
+  }
+  // r in [0, 3 ell): two conditional subtractions
+#pragma unroll
+  for (int rep = 0; rep < 2; rep++) {
+    uint32_t d[L + 1];
+    br = 0;
+#pragma unroll
+    for (int j = 0; j <= L; j++) {
+      int64_t v = (int64_t)r[j] - (j < L ? mp.ell[j] : 0) + br;
+      d[j] = (uint32_t)v;
+      br = v >> 32;
+    }
+    if (br == 0) {
+#pragma unroll
+      for (int j = 0; j <= L; j++) r[j] = d[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < L; j++) R[j] = r[j];
+}
+
+// ------------------------------------------------------------- SpMV pass
+//
+// One thread per output row ("slot" in the sorted SELL-32 order), one warp
+// per 32-slot slice.  Entry streams are laid out [group][lane][4] so every
+// 128-bit index load of a warp is one coalesced 512-byte transaction.
+template <int L, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t slice = slot >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (FIRST && blockIdx.x == 0 && threadIdx.x < a.proj_m) {
+    // a_i = X^T v_i of the iterate this product consumes (solver.py:210)
+    const uint32_t* src = a.x + (size_t)a.proj_rows[threadIdx.x] * SW;
+    uint32_t* dst = a.terms_out + (size_t)threadIdx.x * SW;
+#pragma unroll
+    for (int i = 0; i < SW; i++) dst[i] = i < L ? (src[i] ^ 0x80000000u) : 0u;
+  }
+  if (slice >= a.nslices) return;
+
+  const uint64_t pol = policy_evict_first();
+  const SliceInfo si = a.slices[slice];
+  int64_t acc[L], acc2[L];
+#pragma unroll
+  for (int i = 0; i < L; i++) { acc[i] = 0; acc2[i] = 0; }
+  int64_t Slo = 0, Shi = 0;
+
+  // +-1 entries
+  const uint4* pp = a.pm_idx + si.pm_off + lane;
+#pragma unroll 1
+  for (uint32_t k = 0; k < si.pm_k4; k++) {
+    const uint4 w = ld_stream(pp + (size_t)k * 32, pol);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint32_t u[4][SW];
+#pragma unroll
+    for (int e = 0; e < 4; e++) gather<SW>(a.x + (size_t)(ws[e] & 0x7FFFFFFFu) * SW, u[e]);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int32_t c = 1 - (int32_t)((ws[e] >> 30) & 2u);  // +1 / -1
+      Slo += c;
+#pragma unroll
+      for (int i = 0; i < L; i++) acc[i] += (int64_t)c * (int64_t)(int32_t)u[e][i];
+    }
+  }
+  // small entries: c = c_hi 2^16 + c_lo, |c_lo|, |c_hi| <= 2^15
+  const uint4* sp = a.s_idx + si.s_off + lane;
+  const int4* cp = a.s_coef + si.s_off + lane;
+#pragma unroll 1
+  for (uint32_t k = 0; k < si.s_k4; k++) {
+    const uint4 w = ld_stream(sp + (size_t)k * 32, pol);
+    const int4 cf = ld_stream(cp + (size_t)k * 32, pol);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    const int32_t cs[4] = {cf.x, cf.y, cf.z, cf.w};
+    uint32_t u[4][SW];
+#pragma unroll
+    for (int e = 0; e < 4; e++) gather<SW>(a.x + (size_t)ws[e] * SW, u[e]);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int32_t clo = (int32_t)((uint32_t)cs[e] << 16) >> 16;
+      const int32_t chi = (cs[e] >> 16) + ((cs[e] >> 15) & 1);  // (c - c_lo) / 2^16 without overflow
+      Slo += clo;
+      Shi += chi;
+#pragma unroll
+      for (int i = 0; i < L; i++) {
+        acc[i] += (int64_t)clo * (int64_t)(int32_t)u[e][i];
+        acc2[i] += (int64_t)chi * (int64_t)(int32_t)u[e][i];
+      }
+    }
+  }
+  if (!FIRST) {
+    const uint32_t* pin = a.part_in + (size_t)slot * SW;
+#pragma unroll
+    for (int i = 0; i < L; i++) acc[i] += pin[i];
+  }
+  const int32_t row = LAST ? a.slot_row[slot] : 0;
+  if (LAST && a.has_full) {
+    // full-class coefficients (f*u mod ell by Montgomery: f stored as f R)
+#pragma unroll 1
+    for (uint32_t p = a.full_ptr[slot]; p < a.full_ptr[slot + 1]; p++) {
+      uint32_t u[SW], f[L], r[L];
+      gather<SW>(a.x + (size_t)a.full_col[p] * SW, u);
+#pragma unroll
+      for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; f[i] = a.full_val[(size_t)p * SW + i]; }
+      montmul<L>(f, u, mp, r);
+#pragma unroll
+      for (int i = 0; i < L; i++) acc[i] += r[i];
+    }
+    if (row >= 0) {
+#pragma unroll 1
+      for (int g = 0; g < a.n_dense; g++) {
+        uint32_t u[SW], f[L], r[L];
+        gather<SW>(a.x + (size_t)(a.dense_col0 + g) * SW, u);
+#pragma unroll
+        for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; }
+        // dense values: [g][row], rows padded to nslices*32
+        const uint32_t* dv = a.dense_val + ((size_t)g * (size_t)a.nslices * 32 + (size_t)row) * SW;
+#pragma unroll
+        for (int i = 0; i < L; i++) f[i] = dv[i];
+        montmul<L>(f, u, mp, r);
+#pragma unroll
+        for (int i = 0; i < L; i++) acc[i] += r[i];
+      }
+    }
+  }
+  uint32_t R[L];
+  finalize<L>(acc, acc2, Slo, Shi, mp, R);
+  uint32_t o[SW];
+  if (LAST) {
+    if (row < 0) return;
+#pragma unroll
+    for (int i = 0; i < SW; i++) o[i] = i < L ? (R[i] ^ 0x80000000u) : 0u;
+    store_slot<SW>(a.y + (size_t)row * SW, o);
+  } else {
+#pragma unroll
+    for (int i = 0; i < SW; i++) o[i] = i < L ? R[i] : 0u;
+    store_slot<SW>(a.part_out + (size_t)slot * SW, o);
+  }
+}
+
+// ------------------------------------------------------ conversion kernels
+
+// digit planes (n x P uint64, one 16-bit digit per cell) -> biased slots
+template <int L>
+__global__ void planes_to_slots(const uint64_t* __restrict__ planes, int P, int64_t n,
+                                uint32_t* __restrict__ out) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t* src = planes + (size_t)i * P;
+  uint32_t o[SW];
+#pragma unroll
+  for (int j = 0; j < SW; j++) {
+    uint32_t lo = 2 * j < P ? (uint32_t)(src[2 * j] & 0xFFFF) : 0u;
+    uint32_t hi = 2 * j + 1 < P ? (uint32_t)(src[2 * j + 1] & 0xFFFF) : 0u;
+    o[j] = j < L ? ((lo | (hi << 16)) ^ 0x80000000u) : 0u;
+  }
+  store_slot<SW>(out + (size_t)i * SW, o);
+}
+
+template <int L>
+__global__ void slots_to_planes(const uint32_t* __restrict__ in, int64_t n, int P,
+                                uint64_t* __restrict__ planes) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t* src = in + (size_t)i * SW;
+  uint64_t* dst = planes + (size_t)i * P;
+  for (int d = 0; d < P; d++) {
+    const int j = d >> 1;
+    uint32_t w = j < L ? (src[j] ^ 0x80000000u) : 0u;
+    dst[d] = (d & 1) ? (w >> 16) : (w & 0xFFFF);
+  }
+}
+
+template <int L>
+__global__ void limbs_to_slots(const uint32_t* __restrict__ limbs, int64_t n, uint32_t* __restrict__ out,
+                               uint32_t bias) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t o[SW];
+#pragma unroll
+  for (int j = 0; j < SW; j++) o[j] = j < L ? (limbs[(size_t)i * L + j] ^ bias) : 0u;
+  store_slot<SW>(out + (size_t)i * SW, o);
+}
+
+template <int L>
+__global__ void slots_to_limbs(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ limbs,
+                               uint32_t bias) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+#pragma unroll
+  for (int j = 0; j < L; j++) limbs[(size_t)i * L + j] = in[(size_t)i * SW + j] ^ bias;
+}
+
+// in-place Montgomery conversion f -> f R mod ell = montmul(f, R^2)
+template <int L>
+__global__ void to_montgomery(uint32_t* __restrict__ slots, int64_t n, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t f[L], r[L];
+#pragma unroll
+  for (int j = 0; j < L; j++) f[j] = slots[(size_t)i * SW + j];
+  montmul<L>(f, mp.R2, mp, r);
+#pragma unroll
+  for (int j = 0; j < L; j++) slots[(size_t)i * SW + j] = r[j];
+}
+
+// zero residue in biased form (the padding target slot)
+template <int L>
+__global__ void set_zero_slot(uint32_t* slot) {
+  constexpr int SW = stride_words(L);
+  const int j = threadIdx.x;
+  if (j < SW) slot[j] = j < L ? 0x80000000u : 0u;
+}
+
+}  // namespace sld

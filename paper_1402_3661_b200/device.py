@@ -1,0 +1,243 @@
+"""Device objects over the C ABI: field context, GPU matrix, GPU vector.
+
+Each `DeviceMatrix` owns one `sld_ctx` (one CUDA stream) so multipliers of
+different Krylov chains can run from different host threads at once (the
+reference runs one multiplier per chain thread, sldlag/solver.py:249-251);
+ctypes releases the GIL for the duration of every call.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+from . import _native as N
+from .modring import as_modulus, ints_to_limbs
+
+DEFAULT_DEVICE = int(os.environ.get("SLD_DEVICE", "0"))
+
+
+def _dense_limbs(A, L):
+    """Dense columns of a SparseMatrix-like object as (n_dense, nrows, L)."""
+    dense = list(getattr(A, "dense_cols", None) or [])
+    if not dense:
+        return 0, None
+    out = np.zeros((len(dense), A.nrows, L), dtype=np.uint32)
+    for g, (gidx, col) in enumerate(dense):
+        if int(gidx) != A.ncols + g:
+            raise ValueError("dense columns must occupy the top indices in order")
+        if isinstance(col, np.ndarray) and col.dtype == np.uint32:
+            out[g] = col.reshape(A.nrows, L)
+        else:
+            out[g] = ints_to_limbs(col, L)
+    return len(dense), out
+
+
+def matrix_arrays(A, L):
+    """The SparseMatrix fields (spmatrix.py:77-91) as contiguous arrays."""
+    row_ptr = N.c64(A.row_ptr)
+    nnz = int(row_ptr[-1]) if len(row_ptr) else 0
+    col = N.c32(A.col_idx) if nnz else np.zeros(0, np.int32)
+    tags = np.ascontiguousarray(A.tags, dtype=np.uint8) if nnz else np.zeros(0, np.uint8)
+    small = N.c64(A.small_vals) if nnz else np.zeros(0, np.int64)
+    fv = A.full_vals
+    if isinstance(fv, tuple):  # (positions, limbs) fast form
+        fpos, flimbs = N.c64(fv[0]), N.cu32(fv[1]).reshape(-1, L)
+        order = np.argsort(fpos, kind="stable")
+        fpos, flimbs = np.ascontiguousarray(fpos[order]), np.ascontiguousarray(flimbs[order])
+    else:
+        keys = sorted(int(k) for k in fv)
+        fpos = np.array(keys, dtype=np.int64)
+        flimbs = ints_to_limbs([fv[k] for k in keys], L)
+    n_dense, dense = _dense_limbs(A, L)
+    return row_ptr, col, tags, small, fpos, flimbs, n_dense, dense
+
+
+class Field:
+    """sld_ctx: one prime on one device (the PrimeModulus of the ABI)."""
+
+    def __init__(self, mod, device=None):
+        self.mod = as_modulus(mod)
+        self.device = DEFAULT_DEVICE if device is None else int(device)
+        self.L = self.mod.limbs
+        lib = N.load()
+        ell = ints_to_limbs([self.mod.ell], self.L)[0].copy()
+        h = ctypes.c_void_p()
+        N.check(lib.sld_ctx_create(self.device, N.ptr(ell), self.L, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def sync(self):
+        N.check(N.load().sld_ctx_sync(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.load().sld_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceVector:
+    """A device vector of n residues (biased 32-bit limbs, sector padded)."""
+
+    def __init__(self, field: Field, n: int):
+        self.field = field
+        self.n = int(n)
+        h = ctypes.c_void_p()
+        N.check(N.load().sld_vec_create(field.handle, self.n, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def upload_planes(self, planes):
+        p = np.ascontiguousarray(planes, dtype=np.uint64)
+        if p.ndim != 2 or p.shape[0] != self.n:
+            raise ValueError("plane count mismatch")
+        N.check(N.load().sld_vec_upload_planes(self._h, N.ptr(p), self.n, p.shape[1]))
+
+    def download_planes(self, P):
+        out = np.empty((self.n, P), dtype=np.uint64)
+        N.check(N.load().sld_vec_download_planes(self._h, N.ptr(out), self.n, P))
+        return out
+
+    def upload_limbs(self, limbs):
+        a = N.cu32(limbs)
+        if a.shape != (self.n, self.field.L):
+            raise ValueError(f"limb array shape {a.shape} != {(self.n, self.field.L)}")
+        N.check(N.load().sld_vec_upload_limbs(self._h, N.ptr(a), self.n))
+
+    def download_limbs(self):
+        out = np.empty((self.n, self.field.L), dtype=np.uint32)
+        N.check(N.load().sld_vec_download_limbs(self._h, N.ptr(out), self.n))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.load().sld_vec_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class XBlock:
+    """A dense projection block (m x n residues) resident on the device."""
+
+    def __init__(self, field: Field, x_limbs):
+        x = N.cu32(x_limbs)
+        m, n = x.shape[0], x.shape[1]
+        self.field, self.m, self.n = field, m, n
+        h = ctypes.c_void_p()
+        N.check(N.load().sld_xblock_create(field.handle, N.ptr(x), m, n, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.load().sld_xblock_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceMatrix:
+    """GPU layout of a SparseMatrix (ours or the reference's, duck-typed on
+    the fields of sldlag/spmatrix.py:77-91) -- the replacement of
+    `SparseMatrix.kernel()` / `SpmvKernel` (vecops.py:355-470)."""
+
+    INFO_KEYS = ("nrows", "total_cols", "nnz", "n_pm", "n_small", "n_full", "stripes",
+                 "nslices", "device_bytes", "pad_entries", "L", "stride_words", "max_degree",
+                 "stripe_cols")
+
+    def __init__(self, A, device=None, stripe_cols=0, field=None):
+        self.mod = as_modulus(A.mod)
+        self.field = field or Field(self.mod, device)
+        self.L = self.field.L
+        self.P = self.mod.digits
+        self.nrows = int(A.nrows)
+        self.ncols = int(A.ncols)
+        arrs = matrix_arrays(A, self.L)
+        row_ptr, col, tags, small, fpos, flimbs, n_dense, dense = arrs
+        if row_ptr.shape != (self.nrows + 1,):
+            raise ValueError("row_ptr length must be nrows + 1")
+        self.n_dense = n_dense
+        self.total_cols = self.ncols + n_dense
+        h = ctypes.c_void_p()
+        N.check(N.load().sld_mat_create(
+            self.field.handle, self.nrows, self.ncols, N.ptr(row_ptr), N.ptr(col), N.ptr(tags),
+            N.ptr(small), len(fpos), N.ptr(fpos), N.ptr(flimbs), n_dense,
+            N.ptr(dense) if dense is not None else ctypes.c_void_p(0), int(stripe_cols),
+            ctypes.byref(h)))
+        self._h = h
+        self._tmp = {}
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        out = np.zeros(16, dtype=np.int64)
+        N.check(N.load().sld_mat_info(self._h, N.ptr(out)))
+        return {k: int(v) for k, v in zip(self.INFO_KEYS, out)}
+
+    def vector(self, n=None):
+        return DeviceVector(self.field, self.total_cols if n is None else n)
+
+    def apply_planes(self, planes):
+        """v = A u on digit planes (host in, host out)."""
+        p = np.ascontiguousarray(planes, dtype=np.uint64)
+        if p.ndim != 2 or p.shape[0] != self.total_cols:
+            raise ValueError("plane count mismatch")
+        out = np.empty((self.nrows, p.shape[1]), dtype=np.uint64)
+        N.check(N.load().sld_spmv_planes(self._h, N.ptr(p), N.ptr(out), p.shape[1]))
+        return out
+
+    def spmv(self, vin: DeviceVector, vout: DeviceVector):
+        N.check(N.load().sld_spmv(self._h, vin.handle, vout.handle))
+
+    def krylov_unit(self, v: DeviceVector, rows, steps):
+        rows = N.c64(rows)
+        m = len(rows)
+        terms = np.zeros((int(steps), m, self.L), dtype=np.uint32)
+        N.check(N.load().sld_krylov_unit(self._h, v.handle, N.ptr(rows), m, int(steps),
+                                          N.ptr(terms) if terms.size else ctypes.c_void_p(0)))
+        return terms
+
+    def krylov_dense(self, v: DeviceVector, xb: XBlock, steps):
+        terms = np.zeros((int(steps), xb.m, self.L), dtype=np.uint32)
+        N.check(N.load().sld_krylov_dense(self._h, v.handle, xb._h, int(steps),
+                                           N.ptr(terms) if terms.size else ctypes.c_void_p(0)))
+        return terms
+
+    def bench(self, v: DeviceVector, steps, warmup=3):
+        tot = ctypes.c_double()
+        per = ctypes.c_double()
+        N.check(N.load().sld_bench_spmv(self._h, v.handle, int(steps), int(warmup),
+                                         ctypes.byref(tot), ctypes.byref(per)))
+        return tot.value, per.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.load().sld_mat_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

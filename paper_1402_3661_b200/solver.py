@@ -1,0 +1,303 @@
+"""Block-Wiedemann Krylov driver on the device.
+
+Keeps the reference's plugin protocols and entry points
+(sldlag/solver.py:40-268):
+
+  * multiplier protocol -- `.apply(planes) -> planes`, `.count`, `.size`,
+    `.mod` (SequentialMultiplier solver.py:129-142).  `B200Multiplier` is the
+    drop-in: `block_wiedemann(A, bp, seed, make_mul=lambda j: B200Multiplier(A,
+    device=j % ndev))` runs the reference driver on B200s unchanged.
+  * projection protocol -- `.project(planes) -> list[int]` (UnitRows /
+    DenseRows, solver.py:168-189).
+  * `krylov_column` / `krylov_block` / `krylov_scalar` / `krylov_length` with
+    the same semantics: a_0 = X^T y is taken before the first product and
+    exactly `count` SpMVs run per chain (solver.py:199-217).
+
+The speed comes from `B200Multiplier.krylov`: the whole chain stays on the
+device (ping-pong iterate, unit-X projection fused into the SpMV kernel,
+CUDA-graph replays), and only the m projected terms per step come back.
+`krylov_column` dispatches to it whenever the multiplier has it, and runs the
+chain in chunks that end exactly on checkpoint flush / halt boundaries so the
+`on_step` / `flush` contract (checkpoint.py:177-200) is honoured.
+"""
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .device import DEFAULT_DEVICE, DeviceMatrix, XBlock
+from .modring import (
+    as_modulus, digit_count, ints_to_limbs, ints_to_planes, limbs_to_ints, limbs_to_planes,
+    planes_to_ints, planes_to_limbs,
+)
+
+SAFETY_MARGIN = 32
+
+
+@dataclass(frozen=True)
+class BlockingParams:
+    n: int
+    m: int
+
+    def __post_init__(self):
+        if self.n < 1 or self.m < self.n:
+            raise ValueError("need m >= n >= 1")
+
+    @classmethod
+    def default(cls, n: int) -> "BlockingParams":
+        return cls(n, 2 * n)
+
+
+def krylov_length(N: int, bp, margin: int = SAFETY_MARGIN) -> int:
+    """ceil(N/n) + ceil(N/m) + margin (solver.py:67-68)."""
+    return -(-N // bp.n) + -(-N // bp.m) + margin
+
+
+@dataclass
+class BlockSequence:
+    """Terms a_i as m x n matrices, stored per y-column (solver.py:71-90)."""
+    m: int
+    n: int
+    columns: list
+    spmvs_per_column: list = field(default_factory=list)
+
+    @property
+    def count(self) -> int:
+        return min(len(c) for c in self.columns) if self.columns else 0
+
+    def term(self, i: int):
+        return [[self.columns[j][i][t] for j in range(self.n)] for t in range(self.m)]
+
+    def scalar(self) -> list:
+        assert self.m == 1 and self.n == 1
+        return [v[0] for v in self.columns[0]]
+
+
+# -- projections ------------------------------------------------------------
+
+
+class UnitRows:
+    """x-block of unit vectors: a_i reads m coordinates (solver.py:168-176)."""
+
+    def __init__(self, rows):
+        self.rows = [int(r) for r in rows]
+
+    def project(self, planes) -> list:
+        return planes_to_ints(np.asarray(planes)[self.rows])
+
+
+class DenseRows:
+    """Random dense x-block: a_i[t] = sum_j x_t[j] v[j] (solver.py:179-189).
+    On the device path the block is uploaded once (Montgomery form) and each
+    step's m dot products run as a grid reduction."""
+
+    def __init__(self, vectors, mod):
+        self.vectors = [list(v) for v in vectors]
+        self.mod = as_modulus(mod)
+        self._dev = {}
+
+    def project(self, planes) -> list:
+        ell = self.mod.ell
+        v = planes_to_ints(planes)
+        return [sum(a * b for a, b in zip(x, v)) % ell for x in self.vectors]
+
+    def device_block(self, dm: DeviceMatrix) -> XBlock:
+        key = id(dm.field)
+        xb = self._dev.get(key)
+        if xb is None:
+            L = dm.L
+            x = np.stack([ints_to_limbs(vec, L) for vec in self.vectors]) if self.vectors \
+                else np.zeros((0, dm.total_cols, L), np.uint32)
+            xb = self._dev[key] = XBlock(dm.field, x)
+        return xb
+
+
+# -- multipliers ------------------------------------------------------------
+
+
+class B200Multiplier:
+    """v <- A v on one B200 with an SpMV counter (the multiplier protocol of
+    sldlag/solver.py:129-163).  `A` may be this package's SparseMatrix or the
+    reference's (same fields).  The device matrix is built lazily on first
+    use, so constructing one just to read `.mod` / `.size` is free
+    (block_wiedemann does exactly that, solver.py:609-610)."""
+
+    def __init__(self, A, device=None, stripe_cols=0):
+        if A.nrows != A.ncols + len(getattr(A, "dense_cols", None) or []):
+            raise ValueError("solver needs a square matrix")
+        self.A = A
+        self.size = int(A.nrows)
+        self.mod = A.mod
+        self.device = DEFAULT_DEVICE if device is None else int(device)
+        self.stripe_cols = stripe_cols
+        self.count = 0
+        self._dm = None
+        self._lock = threading.Lock()
+
+    @property
+    def dm(self) -> DeviceMatrix:
+        if self._dm is None:
+            self._dm = DeviceMatrix(self.A, self.device, stripe_cols=self.stripe_cols)
+        return self._dm
+
+    def apply(self, planes):
+        with self._lock:
+            out = self.dm.apply_planes(planes)
+        self.count += 1
+        return out
+
+    def krylov(self, xblock, v_planes, steps):
+        """`steps` chain steps on the device from iterate `v_planes`:
+        returns (terms as list of m-int lists, final iterate planes)."""
+        with self._lock:
+            dm = self.dm
+            P = v_planes.shape[1]
+            vec = dm.vector()
+            vec.upload_planes(v_planes)
+            if isinstance(xblock, UnitRows):
+                terms = dm.krylov_unit(vec, xblock.rows, steps)
+            elif isinstance(xblock, DenseRows) or hasattr(xblock, "vectors"):
+                db = xblock if isinstance(xblock, DenseRows) else DenseRows(xblock.vectors, self.mod)
+                terms = dm.krylov_dense(vec, db.device_block(dm), steps)
+            else:
+                raise TypeError(f"unsupported projection block {type(xblock).__name__}")
+            v_out = vec.download_planes(P)
+            vec.close()
+        self.count += int(steps)
+        m = terms.shape[1]
+        flat = limbs_to_ints(terms.reshape(-1, terms.shape[2])) if terms.size else []
+        out = [flat[i * m:(i + 1) * m] for i in range(int(steps))]
+        return out, v_out
+
+
+# the reference's name for the default multiplier
+SequentialMultiplier = B200Multiplier
+
+
+def _steps_until_flush(checkpoint, j):
+    """How many steps can run before `checkpoint.on_step` could flush or
+    halt (so the device chunk can end exactly there)."""
+    if hasattr(checkpoint, "steps_until_flush"):
+        return max(1, int(checkpoint.steps_until_flush(j)))
+    # the reference CheckpointManager (checkpoint.py:67-200)
+    every = getattr(checkpoint, "every", None)
+    since = getattr(checkpoint, "_since_flush", None)
+    if every is None or since is None:
+        return 1
+    n = int(every) - int(since.get(j, 0))
+    halt = getattr(checkpoint, "halt_after", None)
+    if halt is not None:
+        n = min(n, int(halt) - int(getattr(checkpoint, "_session_steps", 0)))
+    return max(1, n)
+
+
+def krylov_column(mul, xblock, y_planes, count, start_terms=None, checkpoint=None, col_index=0):
+    """One chain: terms[i] = X^T (B^i y) for i < count, exactly count SpMVs
+    (solver.py:199-217).  Device-resident when `mul` has `.krylov`."""
+    terms = list(start_terms) if start_terms else []
+    v = y_planes
+    spmvs = 0
+    if not hasattr(mul, "krylov"):
+        for _ in range(len(terms), count):
+            terms.append(xblock.project(v))
+            v = mul.apply(v)
+            spmvs += 1
+            if checkpoint is not None:
+                checkpoint.on_step(col_index, terms, v)
+    else:
+        remaining = count - len(terms)
+        while remaining > 0:
+            chunk = remaining if checkpoint is None else min(remaining,
+                                                             _steps_until_flush(checkpoint, col_index))
+            new_terms, v = mul.krylov(xblock, v, chunk)
+            spmvs += chunk
+            remaining -= chunk
+            if checkpoint is None:
+                terms.extend(new_terms)
+                continue
+            # replay the per-step hook; only the chunk's last step can flush
+            for t in new_terms:
+                terms.append(t)
+                checkpoint.on_step(col_index, terms, v)
+    if checkpoint is not None and spmvs:
+        checkpoint.flush(col_index, terms, v)
+    return terms, v, spmvs
+
+
+def _as_planes(vec, mod):
+    return ints_to_planes(vec, digit_count(mod.ell))
+
+
+def krylov_block(A, X, Y, count, muls=None, checkpoint=None, contexts=None) -> BlockSequence:
+    """a_i = X^T A^i Y with the n column chains independent
+    (solver.py:220-257).  Default multipliers are B200Multipliers spread
+    round-robin over the visible devices; chains run on host threads."""
+    n = len(Y)
+    if muls is None:
+        from ._native import device_count
+        ndev = max(1, device_count())
+        muls = [B200Multiplier(A, device=j % ndev) for j in range(n)]
+    mod = muls[0].mod
+    if contexts is None:
+        contexts = int(os.environ.get("SLDLAG_CONTEXTS", str(n)))
+
+    def run(j):
+        start = checkpoint.load_column(j) if checkpoint is not None else None
+        if start is not None:
+            terms0, v_planes = start
+            if len(terms0) >= count:
+                return terms0[:count], 0
+        else:
+            terms0, v_planes = [], _as_planes(Y[j], mod)
+        terms, _, spmvs = krylov_column(muls[j], X, v_planes, count, start_terms=terms0,
+                                        checkpoint=checkpoint, col_index=j)
+        return terms, spmvs
+
+    if contexts > 1 and n > 1:
+        with ThreadPoolExecutor(max_workers=contexts) as pool:
+            results = list(pool.map(run, range(n)))
+    else:
+        results = [run(j) for j in range(n)]
+    m = len(results[0][0][0]) if results and results[0][0] else 0
+    return BlockSequence(m=m, n=n, columns=[r[0] for r in results],
+                         spmvs_per_column=[r[1] for r in results])
+
+
+def krylov_scalar(A, x, y, count=None, mul=None) -> list:
+    """a_i = x^T A^i y for i < count (default 2N) (solver.py:260-268)."""
+    if count is None:
+        count = 2 * (A.nrows if A is not None else mul.size)
+    if mul is None:
+        mul = B200Multiplier(A)
+    xb = DenseRows([x], mul.mod)
+    terms, _, _ = krylov_column(mul, xb, _as_planes(y, mul.mod), count)
+    return [t[0] for t in terms]
+
+
+def draw_blocks(mod, size: int, bp, rng, x_mode="unit", forced_zero=()):
+    """Random Y block and projection block (solver.py:578-596): the same
+    draws in the same order, so seeds give the reference's blocks."""
+    mod = as_modulus(mod)
+    fz = set(forced_zero)
+    allowed = [i for i in range(size) if i not in fz]
+    Y = []
+    for _ in range(bp.n):
+        y = mod.random_residues(rng, size)
+        for z in forced_zero:
+            y[z] = 0
+        Y.append(y)
+    if x_mode == "unit":
+        picks = rng.choice(len(allowed), size=bp.m, replace=False)
+        return UnitRows(sorted(allowed[int(r)] for r in picks)), Y
+    if x_mode == "dense":
+        return DenseRows([mod.random_residues(rng, size) for _ in range(bp.m)], mod), Y
+    raise ValueError(f"unknown x_mode {x_mode!r}")
+
+
+__all__ = [
+    "BlockingParams", "BlockSequence", "B200Multiplier", "SequentialMultiplier", "UnitRows",
+    "DenseRows", "krylov_column", "krylov_block", "krylov_scalar", "krylov_length",
+    "draw_blocks", "SAFETY_MARGIN", "planes_to_limbs", "limbs_to_planes",
+]

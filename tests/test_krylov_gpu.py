@@ -1,0 +1,166 @@
+"""Device-resident Krylov chain parity: the cfg1 200-SpMV golden chain of the
+reference (bit-exact terms and final iterate), the reference's Krylov cases
+(unit and dense X, several chains), SpMV counts, checkpoint chunking and
+thread independence."""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import fixture_sparse, rand_matrix, to_oracle
+from paper_1402_3661_b200 import (
+    B200Multiplier, BlockingParams, DenseRows, PrimeModulus, SparseMatrix, UnitRows, draw_blocks,
+    krylov_block, krylov_column, krylov_length, krylov_scalar,
+)
+from paper_1402_3661_b200.modring import digit_count, ints_to_planes, planes_to_ints
+
+pytestmark = pytest.mark.gpu
+
+
+def test_cfg1_golden_200_steps():
+    z = O.load_golden("cfg1.npz")
+    A = fixture_sparse(z, "")
+    y = O.bytes_to_ints(z["y"])
+    X = UnitRows(z["xrows"].tolist())
+    seq = krylov_block(A, X, [y], 200)
+    want = [O.bytes_to_ints(t) for t in z["terms"]]
+    assert seq.columns[0] == want
+    assert seq.spmvs_per_column == [200]
+    mul = B200Multiplier(A)
+    P = digit_count(A.mod.ell)
+    terms, v, spmvs = krylov_column(mul, X, ints_to_planes(y, P), 200)
+    assert spmvs == 200 and mul.count == 200
+    assert planes_to_ints(v) == O.bytes_to_ints(z["v200"])
+    # one product through the plugin's apply() as well
+    m2 = B200Multiplier(A)
+    assert planes_to_ints(m2.apply(ints_to_planes(y, P))) == O.bytes_to_ints(z["v1"])
+    assert m2.count == 1
+
+
+def test_reference_krylov_cases():
+    z = O.load_golden("krylov_cases.npz")
+    for i in range(int(z["ncases"])):
+        p = f"k{i}_"
+        A = fixture_sparse(z, p)
+        count, mode = int(z[p + "count"]), str(z[p + "mode"])
+        Y = [O.bytes_to_ints(y) for y in z[p + "Y"]]
+        if mode == "unit":
+            X = UnitRows(z[p + "xrows"].tolist())
+        else:
+            X = DenseRows([O.bytes_to_ints(x) for x in z[p + "xdense"]], A.mod)
+        seq = krylov_block(A, X, Y, count)
+        for j in range(len(Y)):
+            want = [O.bytes_to_ints(t) for t in z[p + "terms"][j]]
+            assert seq.columns[j] == want, (i, j)
+
+
+@pytest.mark.parametrize("count", [0, 1, 2, 31, 32, 33, 64, 65, 1100])
+def test_chain_lengths_vs_oracle(count):
+    # odd/even lengths cross the CUDA-graph (32 products) and drain (1024) boundaries
+    mod = PrimeModulus(2**200 - 75)
+    rng = np.random.default_rng(count)
+    A = rand_matrix(mod, rng, 90, 89, 9, dense=1)  # square: 89 sparse + 1 dense column
+    y = mod.random_residues(rng, 90)
+    rows = [3, 50, 89]
+    orc = to_oracle(A)
+    ot, ov = O.krylov_unit(orc, O.ints_to_limbs(y, mod.limbs), rows, count)
+    mul = B200Multiplier(A)
+    terms, v, spmvs = krylov_column(mul, UnitRows(rows), ints_to_planes(y, digit_count(mod.ell)), count)
+    assert spmvs == count
+    assert terms == [O.limbs_to_ints(t) for t in ot]
+    assert planes_to_ints(v) == O.limbs_to_ints(ov)
+
+
+def test_dense_x_vs_oracle():
+    mod = PrimeModulus(0xc152a866f35196bb08ec18cd24e7a4f6d2ac709d)
+    rng = np.random.default_rng(11)
+    A = rand_matrix(mod, rng, 300, 300, 12)
+    y = mod.random_residues(rng, 300)
+    X = DenseRows([mod.random_residues(rng, 300) for _ in range(4)], mod)
+    orc = to_oracle(A)
+    x = np.stack([O.ints_to_limbs(v, mod.limbs) for v in X.vectors])
+    ot, _ = O.krylov_dense(orc, O.ints_to_limbs(y, mod.limbs), x, 40)
+    terms, _, _ = krylov_column(B200Multiplier(A), X, ints_to_planes(y, digit_count(mod.ell)), 40)
+    assert terms == [O.limbs_to_ints(t) for t in ot]
+
+
+def test_krylov_scalar_identity_and_zero():
+    mod = PrimeModulus(1009)
+    rng = np.random.default_rng(1)
+    I = SparseMatrix.from_rows(mod, 6, 6, [[(i, 1)] for i in range(6)])
+    x = [int(v) for v in rng.integers(0, 1009, 6)]
+    y = [int(v) for v in rng.integers(0, 1009, 6)]
+    a0 = sum(a * b for a, b in zip(x, y)) % 1009
+    assert krylov_scalar(I, x, y, count=9) == [a0] * 9
+    Z = SparseMatrix.from_rows(mod, 5, 5, [[] for _ in range(5)])
+    assert krylov_scalar(Z, x[:5], y[:5], count=8) == [sum(a * b for a, b in zip(x[:5], y[:5])) % 1009] + [0] * 7
+
+
+def test_spmv_counts_and_column_isolation():
+    mod = PrimeModulus(2**61 - 1)
+    rng = np.random.default_rng(13)
+    A = rand_matrix(mod, rng, 60, 60, 6)
+    bp = BlockingParams(3, 6)
+    X, Y = draw_blocks(mod, 60, bp, rng, "unit")
+    count = krylov_length(60, bp)
+    assert count == 20 + 10 + 32
+    joint = krylov_block(A, X, Y, count)
+    assert joint.spmvs_per_column == [count] * 3
+    for j in range(3):
+        alone = krylov_block(A, X, [Y[j]], count, contexts=1)
+        assert alone.columns[0] == joint.columns[j]
+
+
+class _RecordingCheckpoint:
+    """Minimal checkpoint with the reference's hook contract
+    (checkpoint.py:177-200): flush every `every` steps per column."""
+
+    def __init__(self, every):
+        self.every = every
+        self._since_flush = {}
+        self._session_steps = 0
+        self.halt_after = None
+        self.flushes = []
+
+    def on_step(self, j, terms, v):
+        self._session_steps += 1
+        self._since_flush[j] = self._since_flush.get(j, 0) + 1
+        if self._since_flush[j] >= self.every:
+            self.flush(j, terms, v)
+
+    def flush(self, j, terms, v):
+        self.flushes.append((j, len(terms), planes_to_ints(v)))
+        self._since_flush[j] = 0
+
+
+def test_checkpoint_flushes_carry_exact_iterates():
+    mod = PrimeModulus(2**127 - 1)
+    rng = np.random.default_rng(21)
+    A = rand_matrix(mod, rng, 50, 50, 8)
+    y = mod.random_residues(rng, 50)
+    ck = _RecordingCheckpoint(every=7)
+    P = digit_count(mod.ell)
+    terms, v, _ = krylov_column(B200Multiplier(A), UnitRows([1, 2]), ints_to_planes(y, P), 30,
+                                checkpoint=ck)
+    orc = to_oracle(A)
+    expect_v = O.ints_to_limbs(y, mod.limbs)
+    iterates = []
+    for _ in range(30):
+        expect_v = orc.spmv_limbs(expect_v)
+        iterates.append(O.limbs_to_ints(expect_v))
+    steps_flushed = [n for _, n, _ in ck.flushes]
+    assert steps_flushed == [7, 14, 21, 28, 30]
+    for (_, n, vv) in ck.flushes:
+        assert vv == iterates[n - 1]
+
+
+def test_resume_matches_uninterrupted():
+    mod = PrimeModulus(2**200 - 75)
+    rng = np.random.default_rng(22)
+    A = rand_matrix(mod, rng, 64, 64, 7)
+    y = mod.random_residues(rng, 64)
+    P = digit_count(mod.ell)
+    X = UnitRows([0, 5])
+    full, vfull, _ = krylov_column(B200Multiplier(A), X, ints_to_planes(y, P), 50)
+    part, vpart, _ = krylov_column(B200Multiplier(A), X, ints_to_planes(y, P), 23)
+    rest, vrest, n = krylov_column(B200Multiplier(A), X, vpart, 50, start_terms=part)
+    assert n == 27 and rest == full and np.array_equal(vrest, vfull)
