@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Krylov SpMV hot path (BASELINE.json metric:
+"SpMV/s mod l (ms per iteration) at 1/2/4/8 B200; % of HBM/IMAD roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+
+A step is one exact product v <- A v mod l of one Krylov chain on one GPU
+(all column-stripe passes).  Multi-GPU (torchrun, one process per GPU) runs
+one independent block-Wiedemann chain per rank -- the sequences never
+communicate (sldlag/solver.py:220-257) -- so scaling is weak and there is no
+data-path collective; the barrier and the max-over-ranks timing use
+torch.distributed.
+
+`--impl reference` times the reference's CPU algorithm -- the C restatement
+of sldlag's exact RNS SpMV in oracle/ (the Python reference cannot travel to
+the GPU box) -- on all host cores, each step a bounded row sample of the same
+matrix, rank 0 only.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMV/s mod ℓ (ms per iteration) at 1/2/4/8 B200; % of HBM/IMAD roofline"
+
+CONFIGS = {
+    # BASELINE.json configs; bp = (n, m) blocking of the block Wiedemann run
+    "cfg1": dict(n=20_000, gamma=20, bits=160, bp=(1, 2), steps=2000, warmup=50,
+                 desc="configs[0]: synthetic N=20K, gamma=20, 160-bit l (CPU-oracle case)"),
+    "cfg2": dict(n=650_000, gamma=100, bits=217, bp=(1, 2), steps=1000, warmup=20,
+                 desc="configs[1]: GF(2^619)-scale N=650K FFS profile, 217-bit l, one sequence"),
+    "cfg3": dict(n=3_600_000, gamma=100, bits=202, bp=(8, 16), steps=400, warmup=10,
+                 desc="configs[2]: GF(2^809)-scale N=3.6M FFS profile, 202-bit l, "
+                      "block Wiedemann (8,16), one sequence per GPU"),
+    "cfg5": dict(n=1_000_000, gamma=100, bits=650, bp=(8, 16), steps=200, warmup=10,
+                 desc="configs[4]: wide-prime stress N=1M FFS profile, 650-bit l, one sequence per GPU"),
+}
+DEFAULT_CONFIG = "cfg3"
+
+L2_GATHER_PEAK_GBS = 9200.0  # measured random 32-byte L2 gather rate, profiles/microbench_r01.txt
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def measured_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"), "/root/repo/MEASURED_PEAKS.json"):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                f = [x.strip() for x in out.split(",")]
+                if len(f) >= 7:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_matrix(cfg, log):
+    from paper_1402_3661_b200 import corpus
+    mod = corpus.random_prime(cfg["bits"], np.random.default_rng(1))
+    prof = corpus.CorpusProfile(n=cfg["n"], gamma=cfg["gamma"], seed=1)
+    t = time.time()
+    A, wit = corpus.generate_with_witnesses(prof, mod)
+    log(f"generated N={A.nrows} nnz={len(A.col_idx)} full={len(A.full_vals)} in {time.time() - t:.1f}s")
+    return A, wit, mod
+
+
+def algorithmic_bytes(A, L):
+    """B = 4 Z + 4 Zs + W Zf + 4 (N+1) + 2 N W, W = 4 L."""
+    W = 4 * L
+    Z = len(A.col_idx)
+    Zs = int(np.count_nonzero(A.tags == 2))
+    Zf = len(A.full_vals)
+    N = A.nrows
+    return 4 * Z + 4 * Zs + W * Zf + 4 * (N + 1) + 2 * N * W, Z, Zs, Zf
+
+
+def int_ops(A, L):
+    """O = L Z+-1 + 2L Zs + 4L^2 Zf + 8 L N."""
+    Zpm = int(np.count_nonzero(A.tags <= 1))
+    Zs = int(np.count_nonzero(A.tags == 2))
+    return L * Zpm + 2 * L * Zs + 4 * L * L * len(A.full_vals) + 8 * L * A.nrows
+
+
+def oracle_for(A):
+    import oracle as O
+    from paper_1402_3661_b200.modring import limbs_to_ints
+    L = A.mod.limbs
+    fpos = sorted(A.full_vals)
+    return O.OracleMatrix(A.mod.ell, A.nrows, A.ncols, A.row_ptr, A.col_idx, A.tags, A.small_vals,
+                          fpos, [A.full_vals[p] for p in fpos], None)
+
+
+def cpu_sample(orc, y_limbs, target_s, log):
+    """Time the oracle port on a bounded row sample; returns (SpMV/s, cores,
+    description).  The full-vector RNS conversion (vecops to_limbs) is timed
+    separately and charged once per SpMV."""
+    cores = os.cpu_count() or 1
+    N = orc.nrows
+    t = time.time()
+    orc.spmv_limbs(y_limbs, rows=(0, 0))
+    t_conv = time.time() - t
+    rows = min(N, 2000)
+    while True:
+        t = time.time()
+        orc.spmv_limbs(y_limbs, rows=(0, rows))
+        dt = time.time() - t - t_conv
+        if dt > 0.5 or rows >= N:
+            break
+        rows = min(N, rows * 4)
+    per_row = max(dt, 1e-9) / rows
+    # scale the sample to ~target_s of CPU work
+    rows2 = int(min(N, max(rows, (target_s - t_conv) / per_row)))
+    t = time.time()
+    orc.spmv_limbs(y_limbs, rows=(0, rows2))
+    dt2 = time.time() - t
+    per_row = max(dt2 - t_conv, 1e-9) / rows2
+    spmv_s = t_conv + per_row * N
+    log(f"cpu oracle: {rows2} rows in {dt2:.2f}s (conversion {t_conv:.2f}s) -> {spmv_s:.3f} s/SpMV")
+    return 1.0 / spmv_s, cores, (f"oracle C port, rows [0,{rows2}) of {N} plus the full "
+                                 f"to-RNS conversion, {cores} threads, extrapolated to one SpMV")
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    log = lambda m: print(f"[bench/reference] {m}", file=sys.stderr, flush=True)  # noqa: E731
+    import oracle as O
+    O.build()
+    A, _, mod = build_matrix(cfg, log)
+    orc = oracle_for(A)
+    rng = np.random.default_rng(3)
+    from paper_1402_3661_b200.corpus import _random_residue_limbs
+    y = _random_residue_limbs(rng, A.total_cols, mod)
+    cores = os.cpu_count() or 1
+    N = A.nrows
+    # size each step's row sample so the whole run stays within ~2-3 minutes
+    t = time.time()
+    orc.spmv_limbs(y, rows=(0, 0))
+    t_conv = time.time() - t
+    t = time.time()
+    probe = min(N, 4000)
+    orc.spmv_limbs(y, rows=(0, probe))
+    per_row = max(time.time() - t - t_conv, 1e-9) / probe
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    rows = int(min(N, max(256, (budget - t_conv) / per_row)))
+    for _ in range(args.warmup):
+        orc.spmv_limbs(y, rows=(0, rows))
+    times = []
+    for k in range(args.steps):
+        lo = (k * rows) % max(1, N - rows + 1)
+        t = time.time()
+        orc.spmv_limbs(y, rows=(lo, lo + rows))
+        times.append(time.time() - t)
+    per_step = float(np.median(times))
+    spmv_s = t_conv + (per_step - t_conv) * N / rows
+    value = 1.0 / spmv_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "SpMV/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": spmv_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "exact integer mod l (RNS 31-bit limbs, reference algorithm)",
+        "data": "synthetic (native corpus generator, FFS profile, seed 1)",
+        "config": config_block(args.config, cfg, A, mod, world),
+        "cpu_baseline": {"value": value, "unit": "SpMV/s", "cores": cores, "kind": "port",
+                         "sample": f"{rows} rows per step of {N} (+ the full to-RNS conversion), "
+                                   f"median of {args.steps} steps, extrapolated to one SpMV"},
+        "e2e": {"value": value, "unit": "SpMV/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(name, cfg, A, mod, world):
+    return {"workload": f"{name}: {cfg['desc']}", "N": A.nrows, "nnz": int(len(A.col_idx)),
+            "ell_bits": mod.bit_length, "gamma": cfg["gamma"], "bp": list(cfg["bp"]),
+            "parallelism": f"independent Krylov chains, 1 per GPU x {world}",
+            "l2": "inputs larger than L2 (matrix streams >1 GB/step at cfg3); the iterate vector's "
+                  "reuse across steps is the Krylov recurrence itself"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    args.steps = args.steps or cfg["steps"]
+    args.warmup = max(3, args.warmup if args.warmup is not None else cfg["warmup"])
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))  # noqa: E731
+    from paper_1402_3661_b200 import B200Multiplier, UnitRows, krylov_column
+    from paper_1402_3661_b200 import _native
+    from paper_1402_3661_b200.corpus import _random_residue_limbs
+    from paper_1402_3661_b200.device import DeviceMatrix
+    from paper_1402_3661_b200.modring import digit_count, limbs_to_planes
+    _native.load()
+    A, wit, mod = build_matrix(cfg, log)
+    t = time.time()
+    dm = DeviceMatrix(A, device=local)
+    info = dm.info()
+    log(f"device layout built in {time.time() - t:.1f}s: {info}")
+    L, P = dm.L, digit_count(mod.ell)
+    rng = np.random.default_rng(1000 + rank)
+    y = _random_residue_limbs(rng, A.total_cols, mod)
+    v = dm.vector()
+    v.upload_limbs(y)
+
+    # ---- device-timed region: W untimed, then exactly K products
+    dm.bench(v, args.warmup, 0)
+    if dist is not None:
+        import torch
+        torch.cuda.synchronize()
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        total_ms, per_ms = dm.bench(v, args.steps, 0)
+    if dist is not None:
+        import torch
+        torch.cuda.synchronize()
+        t_all = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        total_ms = float(t_all.item())
+    steps_even = 2 * ((args.steps + 1) // 2)  # the bench graph replays product pairs
+    ms_per_step = total_ms / steps_even
+    value = world * steps_even / (total_ms / 1e3)
+    launches = steps_even * info["stripes"]
+
+    # ---- end to end through the public API: krylov_column with host y in,
+    # host terms (m per step) and the final iterate out
+    bp_m = cfg["bp"][1]
+    X = UnitRows(sorted(int(r) for r in np.random.default_rng(7).choice(A.nrows, bp_m, replace=False)))
+    y_planes = limbs_to_planes(y, P)
+    mul = B200Multiplier(A, device=local, dm=dm)
+    e2e_steps = args.steps
+    if dist is not None:
+        dist.barrier()
+    with ClockSampler(local) as clk_e2e:
+        t0 = time.perf_counter()
+        terms, v_out, spmvs = krylov_column(mul, X, y_planes, e2e_steps)
+        t_e2e = time.perf_counter() - t0
+    if dist is not None:
+        import torch
+        te = torch.tensor([t_e2e], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        t_e2e = float(te.item())
+    e2e_value = world * e2e_steps / t_e2e
+    h2d = y_planes.nbytes + 8 * bp_m
+    d2h = e2e_steps * bp_m * 4 * L + v_out.nbytes
+    # the plain multiplier protocol as well: host planes in/out every product
+    n_apply = 3 if A.nrows > 1_000_000 else 10
+    t0 = time.perf_counter()
+    pl = y_planes
+    for _ in range(n_apply):
+        pl = mul.apply(pl)
+    t_apply = time.perf_counter() - t0
+
+    # ---- kernel correctness spot check at full size: planted witness A w = 0
+    ok_witness = None
+    if wit:
+        from paper_1402_3661_b200.modring import ints_to_planes, planes_to_ints
+        wv = [0] * A.total_cols
+        for c, val in wit[0].items():
+            wv[c] = val
+        ok_witness = not any(planes_to_ints(dm.apply_planes(ints_to_planes(wv, P))))
+
+    # ---- roofline (SURVEY.md 8(d) algorithmic bytes per product)
+    B, Z, Zs, Zf = algorithmic_bytes(A, L)
+    peak, peak_kind = measured_peaks()
+    achieved = B / (ms_per_step / 1e3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get("dram_bytes_per_product")
+    gather_bytes = 32 * ((4 * L + 31) // 32) * (Z + Zf) + B
+    line = {
+        "metric": METRIC, "value": value, "unit": "SpMV/s", "n_gpus": world, "steps": steps_even,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 limbs, exact mod l (int64 lazy accumulation)",
+        "data": "synthetic (native corpus generator, FFS profile, seed 1, planted kernel column)",
+        "config": config_block(args.config, cfg, A, mod, world),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_product": B, "kernel": "spmv_pass (all stripe passes)"},
+        "gather_roofline": {"bound": "l2_random_sector_gather", "peak": L2_GATHER_PEAK_GBS,
+                            "unit": "GB/s", "bytes_per_product": gather_bytes,
+                            "achieved": gather_bytes / (ms_per_step / 1e3) / 1e9,
+                            "frac": gather_bytes / (ms_per_step / 1e3) / 1e9 / L2_GATHER_PEAK_GBS},
+        "int_ops_per_product": int_ops(A, L),
+        "e2e": {"value": e2e_value, "unit": "SpMV/s", "h2d_bytes_per_step": h2d / e2e_steps,
+                "d2h_bytes_per_step": d2h / e2e_steps, "api": "krylov_column(B200Multiplier, UnitRows)",
+                "steps": e2e_steps},
+        "e2e_apply": {"value": world * n_apply / t_apply, "unit": "SpMV/s",
+                      "h2d_bytes_per_step": y_planes.nbytes, "d2h_bytes_per_step": y_planes.nbytes,
+                      "api": "B200Multiplier.apply(planes) per product"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "clocks_e2e": clk_e2e.summary(),
+        "layout": info,
+        "witness_check": ok_witness,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            O.build()
+            orc = oracle_for(A)
+            val, cores, sample = cpu_sample(orc, y, args.cpu_seconds, log)
+            line["cpu_baseline"] = {"value": val, "unit": "SpMV/s", "cores": cores, "kind": "port",
+                                    "sample": sample}
+        except Exception as e:  # the baseline must not hide the GPU number
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

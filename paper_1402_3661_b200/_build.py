@@ -1,23 +1,25 @@
 """Build libsldb200.so in-tree with nvcc for sm_100a (no JIT, no torch
-extension machinery): `python -m paper_1402_3661_b200._build`."""
+extension machinery): `python -m paper_1402_3661_b200._build [--force]`.
+Translation units compile in parallel; the kernel instantiations are split
+by limb count (csrc/sld_inst_*.cu)."""
 import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 OUT_DIR = os.path.join(PKG, "_lib")
+OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libsldb200.so")
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
-    "--expt-relaxed-constexpr", "-cudart", "static",
-]
-SOURCES = ["sld_capi.cu", "sld_corpus.cpp"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+                     "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
+SOURCES = ["sld_capi.cu", "sld_inst_1_8.cu", "sld_inst_9_16.cu", "sld_inst_17_24.cu",
+           "sld_inst_25_32.cu", "sld_corpus.cpp"]
 
 
 def nvcc():
@@ -27,21 +29,36 @@ def nvcc():
     raise RuntimeError("nvcc not found: the CUDA toolkit is required to build libsldb200.so")
 
 
-def _stale():
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+def _newest_dep():
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "sldb200.h")]
-    return any(os.path.getmtime(d) > t for d in deps)
+    return max(os.path.getmtime(d) for d in deps)
+
+
+def _stale():
+    return not os.path.exists(LIB) or _newest_dep() > os.path.getmtime(LIB)
 
 
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    cc = nvcc()
+    newest = _newest_dep()
+
+    def compile_one(src):
+        obj = os.path.join(OBJ_DIR, os.path.splitext(src)[0] + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > newest:
+            return obj
+        cmd = [cc, *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-I", INCLUDE, "-o", tmp,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-lpthread", "-ldl"]
+    cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread", "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
@@ -50,4 +67,4 @@ def build(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -106,12 +106,14 @@ def generate_with_witnesses(profile: CorpusProfile, ell, nthreads: int = 0):
     ncols = n - dc
     row_ptr, col, tags, small = generate_arrays(profile, mod, nthreads)
     rng = np.random.default_rng(np.random.SeedSequence(profile.seed, spawn_key=(0xC0,)))
-    L = mod.limbs
     dense = [(ncols + g, _random_residue_limbs(rng, n, mod)) for g in range(dc)]
     planted = sorted(int(c) for c in rng.choice(ncols, size=profile.planted_kernel_cols,
                                                 replace=False))
-    rows_of = np.repeat(np.arange(n, dtype=np.int64), np.diff(row_ptr))
     pool = np.setdiff1d(np.arange(ncols + dc), np.array(planted))
+
+    def rows_of(pos):
+        return np.searchsorted(row_ptr, pos, side="right") - 1
+
     witnesses, new_entries = [], {}
     for k, t in enumerate(planted):
         a, b = (int(x) for x in rng.choice(pool, size=2, replace=False))
@@ -122,45 +124,61 @@ def generate_with_witnesses(profile: CorpusProfile, ell, nthreads: int = 0):
         combo = {}
         for src, coef in ((a, alpha), (b, beta)):
             if src >= ncols:
-                vals = dense[src - ncols][1]
                 from .modring import limbs_to_ints
-                for i, v in enumerate(limbs_to_ints(vals)):
+                for i, v in enumerate(limbs_to_ints(dense[src - ncols][1])):
                     if v:
                         combo[i] = (combo.get(i, 0) + coef * v) % mod.ell
             else:
                 hit = np.nonzero(col == src)[0]
-                for p in hit.tolist():
-                    i = int(rows_of[p])
+                for i, p in zip(rows_of(hit).tolist(), hit.tolist()):
                     combo[i] = (combo.get(i, 0) + coef * int(small[p])) % mod.ell
         new_entries[t] = {i: v for i, v in combo.items() if v}
         witnesses.append({t: 1, a: (-alpha) % mod.ell, b: (-beta) % mod.ell})
-    # drop the planted columns' original entries, splice the replacements in
-    keep = ~np.isin(col, np.array(planted, dtype=np.int32))
-    rows_k, col_k, tags_k, small_k = rows_of[keep], col[keep], tags[keep], small[keep]
-    er, ec, ev = [], [], []
+    # rewrite only the affected rows: drop the planted columns' entries and
+    # merge the replacement entries in column order
+    pl = np.array(planted, dtype=np.int32)
+    drop_pos = np.nonzero(np.isin(col, pl))[0]
+    affected = set(rows_of(drop_pos).tolist())
     for t in planted:
-        for i, v in sorted(new_entries[t].items()):
-            er.append(i)
-            ec.append(t)
-            ev.append(v)
-    order = np.lexsort((np.array(ec, dtype=np.int64), np.array(er, dtype=np.int64))) if er else []
-    er = np.array(er, dtype=np.int64)[order] if len(er) else np.zeros(0, np.int64)
-    ec = np.array(ec, dtype=np.int64)[order] if len(ec) else np.zeros(0, np.int64)
-    ev = [ev[i] for i in order] if len(order) else []
-    etags = np.empty(len(ev), dtype=np.uint8)
-    esm = np.empty(len(ev), dtype=np.int64)
-    for j, v in enumerate(ev):
-        etags[j], esm[j] = classify(v, mod)
-    key = rows_k * ncols + col_k.astype(np.int64)
-    pos = np.searchsorted(key, er * ncols + ec)
-    all_rows = np.insert(rows_k, pos, er)
-    all_col = np.insert(col_k, pos, ec.astype(np.int32))
-    all_tags = np.insert(tags_k, pos, etags)
-    all_small = np.insert(small_k, pos, esm)
-    final = pos + np.arange(len(ev))
-    fulls = {int(final[j]): v for j, v in enumerate(ev) if etags[j] == TAG_FULL}
+        affected.update(new_entries[t])
+    affected = sorted(affected)
+    pieces = {"col": [], "tags": [], "small": []}
+    fulls_rel = []  # (output position, value)
+    counts = np.diff(row_ptr).copy()
+    out_len = 0
+    prev = 0
+    for r in affected:
+        lo, hi = int(row_ptr[r]), int(row_ptr[r + 1])
+        # untouched stretch [prev, lo)
+        pieces["col"].append(col[prev:lo]); pieces["tags"].append(tags[prev:lo])
+        pieces["small"].append(small[prev:lo]); out_len += lo - prev
+        ents = [(int(c), int(tg), int(sv), None) for c, tg, sv in
+                zip(col[lo:hi].tolist(), tags[lo:hi].tolist(), small[lo:hi].tolist())
+                if c not in planted]
+        for t in planted:
+            v = new_entries[t].get(r)
+            if v:
+                tg, sv = classify(v, mod)
+                ents.append((t, int(tg), int(sv), v if tg == TAG_FULL else None))
+        ents.sort(key=lambda e: e[0])
+        pieces["col"].append(np.array([e[0] for e in ents], dtype=np.int32))
+        pieces["tags"].append(np.array([e[1] for e in ents], dtype=np.uint8))
+        pieces["small"].append(np.array([e[2] for e in ents], dtype=np.int64))
+        for j, e in enumerate(ents):
+            if e[3] is not None:
+                fulls_rel.append((out_len + j, e[3]))
+        out_len += len(ents)
+        counts[r] = len(ents)
+        prev = hi
+    pieces["col"].append(col[prev:]); pieces["tags"].append(tags[prev:])
+    pieces["small"].append(small[prev:])
+    del col, tags, small
+    all_col = np.concatenate(pieces["col"])
+    all_tags = np.concatenate(pieces["tags"])
+    all_small = np.concatenate(pieces["small"])
+    fulls = dict(fulls_rel)
     rp = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(np.bincount(all_rows, minlength=n), out=rp[1:])
+    np.cumsum(counts, out=rp[1:])
     A = SparseMatrix(mod, n, ncols, rp, all_col, all_tags, all_small, fulls, dense, validate=False)
     return A, witnesses
 

@@ -16,8 +16,7 @@
 #include <vector>
 
 #include "../../include/sldb200.h"
-#include "sld_device.cuh"
-#include "sld_dense.cuh"
+#include "sld_ops.cuh"
 
 using namespace sld;
 
@@ -155,6 +154,7 @@ struct sld_mat {
   uint4* s_idx = nullptr;
   int4* s_coef = nullptr;
   int32_t* slot_row = nullptr;
+  uint32_t* lane_k4 = nullptr;  // [pass][slot]
   uint32_t* full_ptr = nullptr;
   uint32_t* full_col = nullptr;
   uint32_t* full_val = nullptr;
@@ -177,66 +177,16 @@ struct sld_mat {
 
 // -------------------------------------------------- per-L dispatch table
 
-struct LOps {
-  void (*pass)(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
-               const ModParams& mp);
-  void (*planes_to_slots)(const uint64_t*, int, int64_t, uint32_t*, cudaStream_t);
-  void (*slots_to_planes)(const uint32_t*, int64_t, int, uint64_t*, cudaStream_t);
-  void (*limbs_to_slots)(const uint32_t*, int64_t, uint32_t*, uint32_t, cudaStream_t);
-  void (*slots_to_limbs)(const uint32_t*, int64_t, uint32_t*, uint32_t, cudaStream_t);
-  void (*to_mont)(uint32_t*, int64_t, const ModParams&, cudaStream_t);
-  void (*zero_slot)(uint32_t*, cudaStream_t);
-  void (*dense_proj)(const DenseProjArgs&, const ModParams&, cudaStream_t);
-};
-
-static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
-
-template <int L>
-struct Ops {
-  static void pass(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
-                   const ModParams& mp) {
-    const unsigned grid = blocks_for(nslices * 32, 256);
-    if (grid == 0) return;
-    if (first && last) spmv_pass<L, true, true><<<grid, 256, 0, s>>>(a, mp);
-    else if (first) spmv_pass<L, true, false><<<grid, 256, 0, s>>>(a, mp);
-    else if (last) spmv_pass<L, false, true><<<grid, 256, 0, s>>>(a, mp);
-    else spmv_pass<L, false, false><<<grid, 256, 0, s>>>(a, mp);
-  }
-  static void p2s(const uint64_t* p, int P, int64_t n, uint32_t* o, cudaStream_t s) {
-    if (n) planes_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(p, P, n, o);
-  }
-  static void s2p(const uint32_t* i, int64_t n, int P, uint64_t* p, cudaStream_t s) {
-    if (n) slots_to_planes<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, P, p);
-  }
-  static void l2s(const uint32_t* l, int64_t n, uint32_t* o, uint32_t b, cudaStream_t s) {
-    if (n) limbs_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(l, n, o, b);
-  }
-  static void s2l(const uint32_t* i, int64_t n, uint32_t* l, uint32_t b, cudaStream_t s) {
-    if (n) slots_to_limbs<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, l, b);
-  }
-  static void mont(uint32_t* x, int64_t n, const ModParams& mp, cudaStream_t s) {
-    if (n) to_montgomery<L><<<blocks_for(n, 128), 128, 0, s>>>(x, n, mp);
-  }
-  static void zero(uint32_t* slot, cudaStream_t s) { set_zero_slot<L><<<1, 32, 0, s>>>(slot); }
-  static void dproj(const DenseProjArgs& a, const ModParams& mp, cudaStream_t s) {
-    dense_project_launch<L>(a, mp, s);
-  }
-  static LOps make() { return LOps{pass, p2s, s2p, l2s, s2l, mont, zero, dproj}; }
-};
-
-template <int L>
-static void fill_ops(LOps* t) {
-  t[L] = Ops<L>::make();
-  if constexpr (L > 1) fill_ops<L - 1>(t);
-}
-
 static const LOps& ops(int L) {
   static LOps table[MAXL + 1];
-  static bool init = false;
-  if (!init) {
-    fill_ops<MAXL>(table);
-    init = true;
-  }
+  static bool init = [] {
+    fill_ops_1_8(table);
+    fill_ops_9_16(table);
+    fill_ops_17_24(table);
+    fill_ops_25_32(table);
+    return true;
+  }();
+  (void)init;
   return table[L];
 }
 
@@ -506,7 +456,7 @@ int dev_upload(T** dst, const std::vector<T>& src, size_t* acct) {
 
 static void mat_free(sld_mat* m) {
   if (!m) return;
-  void* ptrs[] = {m->slices, m->pm_idx, m->s_idx, m->s_coef, m->slot_row, m->full_ptr,
+  void* ptrs[] = {m->slices, m->pm_idx, m->s_idx, m->s_coef, m->slot_row, m->lane_k4, m->full_ptr,
                   m->full_col, m->full_val, m->dense_val, m->part, m->stage, m->proj_rows,
                   m->terms_dev, m->dproj_part};
   for (void* p : ptrs)
@@ -595,6 +545,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
                              "(> 2^15 small or > 2^24 +-1 entries in a row)");
   // ---- slot order: rows sorted by (+-1 count, small count) descending
   std::vector<int64_t> tot_pm(nrows, 0), tot_s(nrows, 0);
+  uint32_t gamma_pm_max = 0, gamma_s_max = 0;
   parallel_for(nrows, [&](int64_t lo, int64_t hi) {
     for (int64_t r = lo; r < hi; r++) {
       int64_t a = 0, b = 0;
@@ -606,6 +557,10 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
       tot_s[r] = b;
     }
   });
+  for (int64_t r = 0; r < nrows; r++) {
+    gamma_pm_max = std::max<uint32_t>(gamma_pm_max, (uint32_t)tot_pm[r]);
+    gamma_s_max = std::max<uint32_t>(gamma_s_max, (uint32_t)tot_s[r]);
+  }
   std::vector<int32_t> order(nrows);
   for (int64_t r = 0; r < nrows; r++) order[r] = (int32_t)r;
   std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
@@ -640,6 +595,16 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
         return fail(SLD_E_BOUND, "matrix too large for 32-bit slice offsets");
     }
   }
+  // per-lane group counts (the SELL slice width is only the max over lanes)
+  std::vector<uint32_t> lane_k4((size_t)npass * nslots, 0);
+  if (std::max(gamma_pm_max, gamma_s_max) >= (1u << 18))
+    return fail(SLD_E_BOUND, "row too long for the per-lane group counter");
+  for (int p = 0; p < npass; p++)
+    for (int64_t slot = 0; slot < nrows; slot++) {
+      const int32_t r = slot_row[slot];
+      const uint32_t a = (rc.pm[(size_t)p * nrows + r] + 3) / 4, b = (rc.sm[(size_t)p * nrows + r] + 3) / 4;
+      lane_k4[(size_t)p * nslots + slot] = a | (b << 16);
+    }
   // ---- entry streams
   std::vector<uint32_t> pm_idx(pm_units * 4, PAD);
   std::vector<uint32_t> s_idx(s_units * 4, PAD);
@@ -711,7 +676,8 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
       }
       for (int q = 0; q < npass; q++) {
         const SliceInfo& si = slices[(size_t)q * nslices + slice];
-        mypads += (int64_t)si.pm_k4 * 4 - kp[q] + (int64_t)si.s_k4 * 4 - ks[q];
+        (void)si;
+        mypads += (int64_t)((kp[q] + 3) / 4) * 4 - kp[q] + (int64_t)((ks[q] + 3) / 4) * 4 - ks[q];
       }
     }
     pads += mypads;
@@ -756,6 +722,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   if (!s_coef.empty()) CU(cudaMemcpy(M->s_coef, s_coef.data(), s_coef.size() * 4, cudaMemcpyHostToDevice));
   acct += pm_idx.size() * 4 + s_idx.size() * 4 + s_coef.size() * 4;
   TRY(dev_upload(&M->slot_row, slot_row, &acct));
+  TRY(dev_upload(&M->lane_k4, lane_k4, &acct));
   TRY(dev_upload(&M->full_ptr, full_ptr, &acct));
   TRY(dev_upload(&M->full_col, full_col, &acct));
   TRY(dev_upload(&M->full_val, full_val, &acct));
@@ -847,12 +814,14 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
     if (proj_m) {
       a.nslices = 0;
       a.slices = M->slices;
+      a.lane_k4 = M->lane_k4;
       o.pass(1, 1, 1, c->stream, a, c->mp);
     }
     return;
   }
   for (int p = 0; p < M->npass; p++) {
     a.slices = M->slices + (size_t)p * M->nslices;
+    a.lane_k4 = M->lane_k4 + (size_t)p * M->nslices * 32;
     o.pass(p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
   }
 }

@@ -46,6 +46,7 @@ struct SpmvArgs {
   const uint4* s_idx;       // small entries: col
   const int4* s_coef;       // small entries: signed coefficient, |c| < 2^31
   const int32_t* slot_row;  // output row of each slot (-1 = padding slot)
+  const uint32_t* lane_k4;  // this pass: per slot (pm groups | small groups << 16)
   // full-class entries and dense columns (last pass only)
   const uint32_t* full_ptr; // per slot, CSR into full_col/full_val
   const uint32_t* full_col;
@@ -253,6 +254,10 @@ __global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModPara
 
   const uint64_t pol = policy_evict_first();
   const SliceInfo si = a.slices[slice];
+  // per-lane group counts: lanes stop at their own row length, so padded
+  // SELL positions are never loaded (no index or gather traffic)
+  const uint32_t kk = a.lane_k4[slot];
+  const uint32_t my_pm = kk & 0xFFFFu, my_s = kk >> 16;
   int64_t acc[L], acc2[L];
 #pragma unroll
   for (int i = 0; i < L; i++) { acc[i] = 0; acc2[i] = 0; }
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModPara
   // +-1 entries
   const uint4* pp = a.pm_idx + si.pm_off + lane;
 #pragma unroll 1
-  for (uint32_t k = 0; k < si.pm_k4; k++) {
+  for (uint32_t k = 0; k < my_pm; k++) {
     const uint4 w = ld_stream(pp + (size_t)k * 32, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
     uint32_t u[4][SW];
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModPara
   const uint4* sp = a.s_idx + si.s_off + lane;
   const int4* cp = a.s_coef + si.s_off + lane;
 #pragma unroll 1
-  for (uint32_t k = 0; k < si.s_k4; k++) {
+  for (uint32_t k = 0; k < my_s; k++) {
     const uint4 w = ld_stream(sp + (size_t)k * 32, pol);
     const int4 cf = ld_stream(cp + (size_t)k * 32, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};

@@ -1,0 +1,71 @@
+// sld_ops.cuh -- per-limb-count kernel dispatch table.  Each translation
+// unit sld_inst_<g>.cu instantiates the kernels for a range of L (so the
+// 32 widths compile in parallel) and fills its slice of the table.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "sld_dense.cuh"
+#include "sld_device.cuh"
+
+namespace sld {
+
+struct LOps {
+  void (*pass)(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
+               const ModParams& mp);
+  void (*planes_to_slots)(const uint64_t*, int, int64_t, uint32_t*, cudaStream_t);
+  void (*slots_to_planes)(const uint32_t*, int64_t, int, uint64_t*, cudaStream_t);
+  void (*limbs_to_slots)(const uint32_t*, int64_t, uint32_t*, uint32_t, cudaStream_t);
+  void (*slots_to_limbs)(const uint32_t*, int64_t, uint32_t*, uint32_t, cudaStream_t);
+  void (*to_mont)(uint32_t*, int64_t, const ModParams&, cudaStream_t);
+  void (*zero_slot)(uint32_t*, cudaStream_t);
+  void (*dense_proj)(const DenseProjArgs&, const ModParams&, cudaStream_t);
+};
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+template <int L>
+struct Ops {
+  static void pass(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
+                   const ModParams& mp) {
+    const unsigned grid = blocks_for(nslices * 32, 256);
+    if (grid == 0) return;
+    if (first && last) spmv_pass<L, true, true><<<grid, 256, 0, s>>>(a, mp);
+    else if (first) spmv_pass<L, true, false><<<grid, 256, 0, s>>>(a, mp);
+    else if (last) spmv_pass<L, false, true><<<grid, 256, 0, s>>>(a, mp);
+    else spmv_pass<L, false, false><<<grid, 256, 0, s>>>(a, mp);
+  }
+  static void p2s(const uint64_t* p, int P, int64_t n, uint32_t* o, cudaStream_t s) {
+    if (n) planes_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(p, P, n, o);
+  }
+  static void s2p(const uint32_t* i, int64_t n, int P, uint64_t* p, cudaStream_t s) {
+    if (n) slots_to_planes<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, P, p);
+  }
+  static void l2s(const uint32_t* l, int64_t n, uint32_t* o, uint32_t b, cudaStream_t s) {
+    if (n) limbs_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(l, n, o, b);
+  }
+  static void s2l(const uint32_t* i, int64_t n, uint32_t* l, uint32_t b, cudaStream_t s) {
+    if (n) slots_to_limbs<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, l, b);
+  }
+  static void mont(uint32_t* x, int64_t n, const ModParams& mp, cudaStream_t s) {
+    if (n) to_montgomery<L><<<blocks_for(n, 128), 128, 0, s>>>(x, n, mp);
+  }
+  static void zero(uint32_t* slot, cudaStream_t s) { set_zero_slot<L><<<1, 32, 0, s>>>(slot); }
+  static void dproj(const DenseProjArgs& a, const ModParams& mp, cudaStream_t s) {
+    dense_project_launch<L>(a, mp, s);
+  }
+  static LOps make() { return LOps{pass, p2s, s2p, l2s, s2l, mont, zero, dproj}; }
+};
+
+template <int L, int LMIN>
+void fill_ops_range(LOps* t) {
+  t[L] = Ops<L>::make();
+  if constexpr (L > LMIN) fill_ops_range<L - 1, LMIN>(t);
+}
+
+// defined in sld_inst_<g>.cu
+void fill_ops_1_8(LOps* t);
+void fill_ops_9_16(LOps* t);
+void fill_ops_17_24(LOps* t);
+void fill_ops_25_32(LOps* t);
+
+}  // namespace sld

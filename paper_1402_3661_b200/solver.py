@@ -124,7 +124,7 @@ class B200Multiplier:
     use, so constructing one just to read `.mod` / `.size` is free
     (block_wiedemann does exactly that, solver.py:609-610)."""
 
-    def __init__(self, A, device=None, stripe_cols=0):
+    def __init__(self, A, device=None, stripe_cols=0, dm=None):
         if A.nrows != A.ncols + len(getattr(A, "dense_cols", None) or []):
             raise ValueError("solver needs a square matrix")
         self.A = A
@@ -133,7 +133,7 @@ class B200Multiplier:
         self.device = DEFAULT_DEVICE if device is None else int(device)
         self.stripe_cols = stripe_cols
         self.count = 0
-        self._dm = None
+        self._dm = dm  # an existing DeviceMatrix of A may be shared
         self._lock = threading.Lock()
 
     @property

@@ -71,7 +71,10 @@ class SparseMatrix:
         self.nrows = int(nrows)
         self.ncols = int(ncols)
         self.row_ptr = np.asarray(row_ptr, dtype=np.int64)
-        self.col_idx = np.asarray(col_idx, dtype=np.int64)
+        col_idx = np.asarray(col_idx)
+        # int32 column indices are kept as-is (no 4-byte-per-entry copy at
+        # N = 3.6M scale); anything else is normalised to the reference's int64
+        self.col_idx = col_idx if col_idx.dtype == np.int32 else col_idx.astype(np.int64)
         self.tags = np.asarray(tags, dtype=np.uint8)
         self.small_vals = np.asarray(small_vals, dtype=np.int64)
         self.full_vals = {int(k): int(v) for k, v in dict(full_vals).items()}
