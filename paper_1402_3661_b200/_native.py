@@ -12,7 +12,7 @@ import numpy as np
 
 from . import _build
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("SLD_LIB", _build.LIB)  # SLD_LIB: experiment builds only
 
 SLD_OK = 0
 SLD_E_ARG = -1

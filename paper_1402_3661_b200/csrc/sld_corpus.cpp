@@ -18,7 +18,7 @@
 #include <thread>
 #include <vector>
 
-#include "../../include/sldb200.h"
+#include "sldb200.h"
 
 namespace {
 

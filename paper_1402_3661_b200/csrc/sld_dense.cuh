@@ -67,16 +67,16 @@ __global__ void dense_proj_final(const DenseProjArgs a, const ModParams mp) {
   constexpr int SW = stride_words(L);
   const int t = blockIdx.x;
   if (threadIdx.x != 0) return;
-  int64_t acc[L], zero[L];
+  int64_t acc[L + 1];
 #pragma unroll
   for (int i = 0; i < L; i++) {
     uint64_t s = 0;
     for (int b = 0; b < a.nblocks; b++) s += a.part[((size_t)t * a.nblocks + b) * MAXL + i];
     acc[i] = (int64_t)s;
-    zero[i] = 0;
   }
+  acc[L] = 0;
   uint32_t R[L];
-  finalize<L>(acc, zero, 0, 0, mp, R);
+  finalize<L>(acc, 0, mp, R);
 #pragma unroll
   for (int i = 0; i < SW; i++) a.out[(size_t)t * SW + i] = i < L ? R[i] : 0u;
 }

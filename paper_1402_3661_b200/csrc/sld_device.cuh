@@ -60,9 +60,17 @@ struct SpmvArgs {
   uint32_t* terms_out;      // proj_m slots of SW words, canonical (unbiased)
   int64_t nslices;
   int has_full;
+  int policy;  // bit0 gather L2 evict_last, bit1 output store evict_first,
+               // bit2 partial store evict_first, bit3 gathers L1::no_allocate
 };
 
 // ---------------------------------------------------------------- loads
+
+__device__ __forceinline__ uint64_t createpolicy_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
@@ -81,6 +89,45 @@ __device__ __forceinline__ T ld_stream(const T* a, uint64_t pol) {
   uint32_t* w = reinterpret_cast<uint32_t*>(&v);
   w[0] = r0; w[1] = r1; w[2] = r2; w[3] = r3;
   return v;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// gather one residue slot with an explicit L2 policy
+template <int SW>
+__device__ __forceinline__ void gather_hint(const uint32_t* __restrict__ p, uint32_t (&u)[SW], uint64_t pol) {
+#pragma unroll
+  for (int q = 0; q < SW / 8; q++) {
+    asm("ld.global.nc.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=r"(u[8 * q + 0]), "=r"(u[8 * q + 1]), "=r"(u[8 * q + 2]), "=r"(u[8 * q + 3]),
+          "=r"(u[8 * q + 4]), "=r"(u[8 * q + 5]), "=r"(u[8 * q + 6]), "=r"(u[8 * q + 7])
+        : "l"(p + 8 * q), "l"(pol));
+  }
+}
+
+template <int SW>
+__device__ __forceinline__ void store_slot_hint(uint32_t* p, const uint32_t (&u)[SW], uint64_t pol) {
+#pragma unroll
+  for (int q = 0; q < SW / 8; q++) {
+    asm volatile("st.global.L2::cache_hint.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p + 8 * q),
+                 "r"(u[8 * q + 0]), "r"(u[8 * q + 1]), "r"(u[8 * q + 2]), "r"(u[8 * q + 3]),
+                 "r"(u[8 * q + 4]), "r"(u[8 * q + 5]), "r"(u[8 * q + 6]), "r"(u[8 * q + 7]), "l"(pol));
+  }
+}
+
+template <int SW>
+__device__ __forceinline__ void load_slot(const uint32_t* __restrict__ p, uint32_t (&u)[SW], uint64_t pol) {
+#pragma unroll
+  for (int q = 0; q < SW / 8; q++) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=r"(u[8 * q + 0]), "=r"(u[8 * q + 1]), "=r"(u[8 * q + 2]), "=r"(u[8 * q + 3]),
+          "=r"(u[8 * q + 4]), "=r"(u[8 * q + 5]), "=r"(u[8 * q + 6]), "=r"(u[8 * q + 7])
+        : "l"(p + 8 * q), "l"(pol));
+  }
 }
 
 // gather one residue slot (SW words, 32-byte sectors) through L1/L2
@@ -151,27 +198,24 @@ __device__ __forceinline__ void montmul(const uint32_t* a, const uint32_t* b, co
   for (int j = 0; j < L; j++) r[j] = ge ? d[j] : t[j];
 }
 
-// Reduce the row value V = sum_i 2^(32i) (a_i + 2^16 b_i) to [0, ell).
-// a_i = acc_i + 2^31 Slo, b_i = acc2_i + 2^31 Shi; |V| < 2^47 ell by the
-// per-row count bounds enforced at build time.
+// Reduce the row value to [0, ell).  The row value is
+//   V = sum_{i<=L} acc_i 2^(32 i) + 2^31 S sum_{i<L} 2^(32 i)
+// (acc_i: per-limb lazy sums of c * (u_i - 2^31), small products split into
+// their 32-bit halves; S = sum of the coefficients: the bias correction).
+// |V| < 2^47 ell by the per-row count bounds enforced at build time.
 template <int L>
-__device__ __forceinline__ void finalize(const int64_t (&acc)[L], const int64_t (&acc2)[L],
-                                         int64_t Slo, int64_t Shi, const ModParams& mp,
+__device__ __forceinline__ void finalize(int64_t (&acc)[L + 1], int64_t S, const ModParams& mp,
                                          uint32_t (&R)[L]) {
+  // bias: 2^31 S = (S >> 1) 2^32 + (S & 1) 2^31, added to every limb i < L
+  const int64_t b_lo = (S & 1) << 31, b_hi = S >> 1;
   uint32_t w[L + 2];
-  const int64_t blo = Slo * ((int64_t)1 << 31), bhi = Shi * ((int64_t)1 << 31);
-  int64_t carry = 0, prev_hi = 0;
+  int64_t carry = 0;
 #pragma unroll
   for (int i = 0; i < L + 2; i++) {
-    int64_t t = carry + prev_hi;
-    if (i < L) {
-      const int64_t a = acc[i] + blo;
-      const int64_t b = acc2[i] + bhi;
-      t += a + ((b & 0xFFFF) << 16);
-      prev_hi = b >> 16;
-    } else {
-      prev_hi = 0;
-    }
+    int64_t t = carry;
+    if (i <= L) t += acc[i];
+    if (i < L) t += b_lo;
+    if (i >= 1 && i <= L) t += b_hi;
     w[i] = (uint32_t)t;
     carry = t >> 32;
   }
@@ -236,8 +280,13 @@ __device__ __forceinline__ void finalize(const int64_t (&acc)[L], const int64_t 
 // One thread per output row ("slot" in the sorted SELL-32 order), one warp
 // per 32-slot slice.  Entry streams are laid out [group][lane][4] so every
 // 128-bit index load of a warp is one coalesced 512-byte transaction.
+// resident CTAs per SM the register allocation must allow: 4 x 256 threads
+// (64 registers) for L <= 8 -- the gathers need every warp they can get
+template <int L>
+constexpr int spmv_min_blocks() { return L <= 8 ? 4 : (L <= 16 ? 2 : 1); }
+
 template <int L, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModParams mp) {
+__global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const SpmvArgs a, const ModParams mp) {
   constexpr int SW = stride_words(L);
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t slice = slot >> 5;
@@ -253,15 +302,16 @@ __global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModPara
   if (slice >= a.nslices) return;
 
   const uint64_t pol = policy_evict_first();
+  const uint64_t gpol = (a.policy & 1) ? policy_evict_last() : createpolicy_normal();
   const SliceInfo si = a.slices[slice];
   // per-lane group counts: lanes stop at their own row length, so padded
   // SELL positions are never loaded (no index or gather traffic)
   const uint32_t kk = a.lane_k4[slot];
   const uint32_t my_pm = kk & 0xFFFFu, my_s = kk >> 16;
-  int64_t acc[L], acc2[L];
+  int64_t acc[L + 1];
 #pragma unroll
-  for (int i = 0; i < L; i++) { acc[i] = 0; acc2[i] = 0; }
-  int64_t Slo = 0, Shi = 0;
+  for (int i = 0; i <= L; i++) acc[i] = 0;
+  int64_t S = 0;  // sum of coefficients (bias correction)
 
   // +-1 entries
   const uint4* pp = a.pm_idx + si.pm_off + lane;
@@ -271,16 +321,17 @@ __global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModPara
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
     uint32_t u[4][SW];
 #pragma unroll
-    for (int e = 0; e < 4; e++) gather<SW>(a.x + (size_t)(ws[e] & 0x7FFFFFFFu) * SW, u[e]);
+    for (int e = 0; e < 4; e++) gather_hint<SW>(a.x + (size_t)(ws[e] & 0x7FFFFFFFu) * SW, u[e], gpol);
 #pragma unroll
     for (int e = 0; e < 4; e++) {
       const int32_t c = 1 - (int32_t)((ws[e] >> 30) & 2u);  // +1 / -1
-      Slo += c;
+      S += c;
 #pragma unroll
       for (int i = 0; i < L; i++) acc[i] += (int64_t)c * (int64_t)(int32_t)u[e][i];
     }
   }
-  // small entries: c = c_hi 2^16 + c_lo, |c_lo|, |c_hi| <= 2^15
+  // small entries: one signed IMAD.WIDE per limb, the 64-bit product split
+  // into its low word (limb i) and signed high word (limb i+1)
   const uint4* sp = a.s_idx + si.s_off + lane;
   const int4* cp = a.s_coef + si.s_off + lane;
 #pragma unroll 1
@@ -291,22 +342,21 @@ __global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModPara
     const int32_t cs[4] = {cf.x, cf.y, cf.z, cf.w};
     uint32_t u[4][SW];
 #pragma unroll
-    for (int e = 0; e < 4; e++) gather<SW>(a.x + (size_t)ws[e] * SW, u[e]);
+    for (int e = 0; e < 4; e++) gather_hint<SW>(a.x + (size_t)ws[e] * SW, u[e], gpol);
 #pragma unroll
     for (int e = 0; e < 4; e++) {
-      const int32_t clo = (int32_t)((uint32_t)cs[e] << 16) >> 16;
-      const int32_t chi = (cs[e] >> 16) + ((cs[e] >> 15) & 1);  // (c - c_lo) / 2^16 without overflow
-      Slo += clo;
-      Shi += chi;
+      S += cs[e];
 #pragma unroll
       for (int i = 0; i < L; i++) {
-        acc[i] += (int64_t)clo * (int64_t)(int32_t)u[e][i];
-        acc2[i] += (int64_t)chi * (int64_t)(int32_t)u[e][i];
+        const int64_t p = (int64_t)cs[e] * (int64_t)(int32_t)u[e][i];
+        acc[i] += (int64_t)(uint32_t)p;
+        acc[i + 1] += (int64_t)(int32_t)(p >> 32);
       }
     }
   }
   if (!FIRST) {
-    const uint32_t* pin = a.part_in + (size_t)slot * SW;
+    uint32_t pin[SW];
+    load_slot<SW>(a.part_in + (size_t)slot * SW, pin, pol);
 #pragma unroll
     for (int i = 0; i < L; i++) acc[i] += pin[i];
   }
@@ -341,17 +391,19 @@ __global__ void __launch_bounds__(256) spmv_pass(const SpmvArgs a, const ModPara
     }
   }
   uint32_t R[L];
-  finalize<L>(acc, acc2, Slo, Shi, mp, R);
+  finalize<L>(acc, S, mp, R);
   uint32_t o[SW];
   if (LAST) {
     if (row < 0) return;
 #pragma unroll
     for (int i = 0; i < SW; i++) o[i] = i < L ? (R[i] ^ 0x80000000u) : 0u;
-    store_slot<SW>(a.y + (size_t)row * SW, o);
+    if (a.policy & 2) store_slot_hint<SW>(a.y + (size_t)row * SW, o, pol);
+    else store_slot<SW>(a.y + (size_t)row * SW, o);
   } else {
 #pragma unroll
     for (int i = 0; i < SW; i++) o[i] = i < L ? R[i] : 0u;
-    store_slot<SW>(a.part_out + (size_t)slot * SW, o);
+    if (a.policy & 4) store_slot_hint<SW>(a.part_out + (size_t)slot * SW, o, pol);
+    else store_slot<SW>(a.part_out + (size_t)slot * SW, o);
   }
 }
 

@@ -1,0 +1,47 @@
+"""Layout / cache-policy sweep on one generated configuration
+(python tools/sweep.py --config cfg3 --policies 0,6 --stripes 0,1800000)."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1402_3661_b200.corpus import _random_residue_limbs  # noqa: E402
+from paper_1402_3661_b200.device import DeviceMatrix  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--policies", default="6")
+    ap.add_argument("--stripes", default="0")
+    a = ap.parse_args()
+    cfg = bench.CONFIGS[a.config]
+    A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
+    y = _random_residue_limbs(np.random.default_rng(5), A.total_cols, mod)
+    for sc in [int(x) for x in a.stripes.split(",")]:
+        for pol in [int(x) for x in a.policies.split(",")]:
+            os.environ["SLD_POLICY"] = str(pol)
+            dm = DeviceMatrix(A, stripe_cols=sc)
+            v = dm.vector()
+            v.upload_limbs(y)
+            dm.bench(v, 10, 0)
+            tot, per = dm.bench(v, a.steps, 0)
+            tot2, per2 = dm.bench(v, a.steps, 0)
+            per = min(per, per2)
+            import subprocess
+            clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.mem,power.draw,temperature.gpu",
+                                  "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
+            print(f"{a.config} stripes={dm.info()['stripes']} policy={pol}: {per:.4f} ms/product  [{clk}]",
+                  flush=True)
+            v.close()
+            dm.close()
+
+
+if __name__ == "__main__":
+    main()
