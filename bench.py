@@ -40,6 +40,9 @@ CONFIGS = {
     "cfg3": dict(n=3_600_000, gamma=100, bits=202, bp=(8, 16), steps=400, warmup=10,
                  desc="configs[2]: GF(2^809)-scale N=3.6M FFS profile, 202-bit l, "
                       "block Wiedemann (8,16), one sequence per GPU"),
+    "cfg4": dict(n=3_600_000, gamma=100, bits=202, bp=(1, 2), steps=100, warmup=5,
+                 desc="configs[3]: the cfg3 matrix, ONE sequence row/2D-partitioned over the GPUs "
+                      "(grid r x c, NCCL exchange)"),
     "cfg5": dict(n=1_000_000, gamma=100, bits=650, bp=(8, 16), steps=200, warmup=10,
                  desc="configs[4]: wide-prime stress N=1M FFS profile, 650-bit l, one sequence per GPU"),
 }
@@ -223,6 +226,63 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_grid(args, cfg, rank, world, local, dist, log):
+    """cfg4: one chain over an r x c grid (strong scaling); device-timed with
+    CUDA events on the stream all grid work runs on, max over ranks."""
+    import torch
+    import torch.distributed as tdist
+    from paper_1402_3661_b200.balance import GridSpec, balance_permutation
+    from paper_1402_3661_b200.corpus import _random_residue_limbs
+    from paper_1402_3661_b200.grid import B200Grid, GridComm
+    if dist is None:
+        tdist.init_process_group("nccl" if torch.cuda.is_available() else "gloo",
+                                 init_method="tcp://127.0.0.1:29533", rank=0, world_size=1)
+    g = GridSpec.parse(args.grid) if args.grid else GridSpec(world, 1)
+    A, _, mod = build_matrix(cfg, log)
+    t = time.time()
+    perm = balance_permutation(A, g)
+    grid = B200Grid(A, g, GridComm(g), device=local, perm=perm)
+    log(f"grid {g} node {(grid.i, grid.j)} block built in {time.time() - t:.1f}s")
+    y = _random_residue_limbs(np.random.default_rng(3), grid.n_padded, mod)
+    grid.load_vector(y)
+    grid.iterate(args.warmup)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        grid.iterate(args.steps)
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t_all = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    tdist.all_reduce(t_all, op=tdist.ReduceOp.MAX)
+    ms = float(t_all.item())
+    last = grid.comm_log.entries[-1]
+    B, Z, Zs, Zf = algorithmic_bytes(A, mod.limbs)
+    peak, peak_kind = measured_peaks()
+    per = ms / args.steps
+    line = {
+        "metric": METRIC, "value": args.steps / (ms / 1e3), "unit": "SpMV/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32 limbs, exact mod l",
+        "data": "synthetic (native corpus generator, FFS profile, seed 1)",
+        "config": dict(config_block("cfg4", cfg, A, mod, world), grid=str(g),
+                       parallelism=f"one chain on a {g} grid (NCCL p2p / all-gather)"),
+        "roofline": {"bound": "hbm", "achieved": B / world / (per / 1e3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": B / world / (per / 1e3) / 1e9 / peak, "traffic": None,
+                     "peak_kind": peak_kind},
+        "comm": {"bytes_per_iter_reference_accounting": last.total_bytes,
+                 "wire_bytes_per_iter": last.reduce.wire_bytes + last.broadcast.wire_bytes,
+                 "messages_per_iter": last.reduce.messages + last.broadcast.messages},
+        "gpu_launches": args.steps * (grid.engine.dm.info()["stripes"] + (1 if g.c > 1 else 0)),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def config_block(name, cfg, A, mod, world):
     return {"workload": f"{name}: {cfg['desc']}", "N": A.nrows, "nnz": int(len(A.col_idx)),
             "ell_bits": mod.bit_length, "gamma": cfg["gamma"], "bp": list(cfg["bp"]),
@@ -240,6 +300,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--grid", default=None, help="cfg4 grid RxC (default: <gpus>x1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     args.steps = args.steps or cfg["steps"]
@@ -260,6 +321,12 @@ def main():
         return
 
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))  # noqa: E731
+    if args.config == "cfg4":
+        run_grid(args, cfg, rank, world, local, dist, log)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     from paper_1402_3661_b200 import B200Multiplier, UnitRows, krylov_column
     from paper_1402_3661_b200 import _native
     from paper_1402_3661_b200.corpus import _random_residue_limbs

@@ -60,6 +60,10 @@ int sld_device_count(int *out);
 int sld_ctx_create(int device, const uint32_t *ell_limbs, int L, sld_ctx **out);
 int sld_ctx_destroy(sld_ctx *ctx);
 int sld_ctx_sync(sld_ctx *ctx);
+/* Run this context's work on an external CUDA stream (e.g. torch's current
+ * stream, so NCCL collectives order with our kernels); 0 restores the
+ * context's own stream. */
+int sld_ctx_set_stream(sld_ctx *ctx, uint64_t cuda_stream);
 
 /*
  * Matrix upload + GPU layout build.  Replaces SparseMatrix.kernel() /
@@ -77,7 +81,7 @@ int sld_ctx_sync(sld_ctx *ctx);
  * max_stripe_cols: column-stripe width for L2 residency of the gathered
  *   vector (0 = automatic, from the device's L2 size).
  * Errors: SLD_E_ARG for inconsistent CSR (spmatrix.py:93-126 checks),
- * SLD_E_BOUND if a row has more than 2^15 small-class or 2^24 +-1 entries.
+ * SLD_E_BOUND if a row has more than 2^15 small-class or 2^18 +-1 entries.
  */
 int sld_mat_create(sld_ctx *ctx, int64_t nrows, int64_t ncols,
                    const int64_t *row_ptr, const int32_t *col_idx,
@@ -104,6 +108,18 @@ int sld_vec_upload_limbs(sld_vec *v, const uint32_t *limbs, int64_t n);
 int sld_vec_download_limbs(sld_vec *v, uint32_t *limbs, int64_t n);
 /* raw device pointer + stride (words) -- for collectives and tests */
 int sld_vec_device_ptr(sld_vec *v, uint64_t *ptr, int64_t *stride_words);
+
+/*
+ * dst = (src_0 + ... + src_{k-1}) mod l over n residues in the device slot
+ * format (sld_vec_device_ptr), 1 <= k <= 64.  Replaces planes_add_mod
+ * (vecops.py:261-264) -- the grid's reduce phase (gridmv.py:291-294) and
+ * the Mksol combination (solver.py:530-536).  Raw device pointers passed as
+ * uint64; dst may alias src_0.
+ */
+int sld_add_mod(sld_ctx *ctx, const uint64_t *src_ptrs, int k, uint64_t dst_ptr, int64_t n);
+
+/* Read m residues (rows[t] of the vector) as canonical limbs (m x L). */
+int sld_vec_read_rows(sld_vec *v, const int64_t *rows, int m, uint32_t *limbs);
 
 /*
  * out = A * in (mod l), canonical.  Replaces SpmvKernel.apply

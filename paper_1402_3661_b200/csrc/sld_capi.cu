@@ -118,7 +118,8 @@ struct sld_ctx {
   int dev = 0;
   int L = 0;
   int SW = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // the stream all work is issued on
+  cudaStream_t own = nullptr;      // the context's own stream
   ModParams mp;
   size_t l2_bytes = 0;
   int sms = 0;
@@ -266,7 +267,8 @@ extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_
   CU(cudaGetDeviceProperties(&pr, device));
   c->l2_bytes = pr.l2CacheSize;
   c->sms = pr.multiProcessorCount;
-  CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  c->stream = c->own;
   *out = c.release();
   return SLD_OK;
 }
@@ -274,13 +276,36 @@ extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_
 extern "C" int sld_ctx_destroy(sld_ctx* c) {
   if (!c) return SLD_OK;
   cudaSetDevice(c->dev);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return SLD_OK;
 }
 
 extern "C" int sld_ctx_sync(sld_ctx* c) {
   CU(cudaSetDevice(c->dev));
+  CU(cudaStreamSynchronize(c->stream));
+  return SLD_OK;
+}
+
+extern "C" int sld_ctx_set_stream(sld_ctx* c, uint64_t stream) {
+  if (!c) return fail(SLD_E_ARG, "null context");
+  CU(cudaSetDevice(c->dev));
+  CU(cudaStreamSynchronize(c->stream));
+  c->stream = stream ? (cudaStream_t)(uintptr_t)stream : c->own;
+  return SLD_OK;
+}
+
+extern "C" int sld_add_mod(sld_ctx* c, const uint64_t* src_ptrs, int k, uint64_t dst_ptr, int64_t n) {
+  if (!c || !src_ptrs || k < 1 || k > 64 || n < 0 || !dst_ptr) return fail(SLD_E_ARG, "bad add_mod arguments");
+  CU(cudaSetDevice(c->dev));
+  AddModArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int i = 0; i < k; i++) a.src[i] = (const uint32_t*)(uintptr_t)src_ptrs[i];
+  a.dst = (uint32_t*)(uintptr_t)dst_ptr;
+  a.k = k;
+  a.n = n;
+  ops(c->L).add_mod(a, c->mp, c->stream);
+  CU(cudaGetLastError());
   CU(cudaStreamSynchronize(c->stream));
   return SLD_OK;
 }
@@ -415,6 +440,27 @@ extern "C" int sld_vec_download_limbs(sld_vec* v, uint32_t* limbs, int64_t n) {
   cudaError_t e = cudaStreamSynchronize(c->stream);
   cudaFree(d);
   if (e != cudaSuccess) return fail(SLD_E_CUDA, "download: %s", cudaGetErrorString(e));
+  return SLD_OK;
+}
+
+extern "C" int sld_vec_read_rows(sld_vec* v, const int64_t* rows, int m, uint32_t* limbs) {
+  if (!v || m < 0 || (m && (!rows || !limbs))) return fail(SLD_E_ARG, "bad read_rows arguments");
+  for (int t = 0; t < m; t++)
+    if (rows[t] < 0 || rows[t] >= v->n) return fail(SLD_E_ARG, "row out of range");
+  if (!m) return SLD_OK;
+  sld_ctx* c = v->ctx;
+  CU(cudaSetDevice(c->dev));
+  int64_t* drows = nullptr;
+  uint32_t* dout = nullptr;
+  CU(cudaMalloc(&drows, m * 8));
+  CU(cudaMalloc(&dout, (size_t)m * c->L * 4));
+  cudaMemcpyAsync(drows, rows, m * 8, cudaMemcpyHostToDevice, c->stream);
+  ops(c->L).read_rows(v->buf[v->cur], drows, m, dout, c->stream);
+  cudaMemcpyAsync(limbs, dout, (size_t)m * c->L * 4, cudaMemcpyDeviceToHost, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaFree(drows);
+  cudaFree(dout);
+  if (e != cudaSuccess) return fail(SLD_E_CUDA, "read_rows: %s", cudaGetErrorString(e));
   return SLD_OK;
 }
 

@@ -478,6 +478,47 @@ __global__ void to_montgomery(uint32_t* __restrict__ slots, int64_t n, const Mod
   for (int j = 0; j < L; j++) slots[(size_t)i * SW + j] = r[j];
 }
 
+// dst = sum_k src_k mod ell over n slots (biased format); k <= 64 so the
+// per-limb sums stay below 2^38 and the row value below 2^47 ell
+struct AddModArgs {
+  const uint32_t* src[64];
+  uint32_t* dst;
+  int k;
+  int64_t n;
+};
+
+template <int L>
+__global__ void add_mod_kernel(const AddModArgs a, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  int64_t acc[L + 1];
+#pragma unroll
+  for (int j = 0; j <= L; j++) acc[j] = 0;
+  for (int s = 0; s < a.k; s++) {
+    const uint32_t* p = a.src[s] + (size_t)i * SW;
+#pragma unroll
+    for (int j = 0; j < L; j++) acc[j] += p[j] ^ 0x80000000u;
+  }
+  uint32_t R[L];
+  finalize<L>(acc, 0, mp, R);
+  uint32_t o[SW];
+#pragma unroll
+  for (int j = 0; j < SW; j++) o[j] = j < L ? (R[j] ^ 0x80000000u) : 0u;
+  store_slot<SW>(a.dst + (size_t)i * SW, o);
+}
+
+// out[t] = canonical limbs of slot rows[t]
+template <int L>
+__global__ void read_rows_kernel(const uint32_t* __restrict__ v, const int64_t* __restrict__ rows, int m,
+                                 uint32_t* __restrict__ out) {
+  constexpr int SW = stride_words(L);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+#pragma unroll
+  for (int j = 0; j < L; j++) out[(size_t)t * L + j] = v[(size_t)rows[t] * SW + j] ^ 0x80000000u;
+}
+
 // zero residue in biased form (the padding target slot)
 template <int L>
 __global__ void set_zero_slot(uint32_t* slot) {

@@ -19,6 +19,8 @@ struct LOps {
   void (*to_mont)(uint32_t*, int64_t, const ModParams&, cudaStream_t);
   void (*zero_slot)(uint32_t*, cudaStream_t);
   void (*dense_proj)(const DenseProjArgs&, const ModParams&, cudaStream_t);
+  void (*add_mod)(const AddModArgs&, const ModParams&, cudaStream_t);
+  void (*read_rows)(const uint32_t*, const int64_t*, int, uint32_t*, cudaStream_t);
 };
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -53,7 +55,13 @@ struct Ops {
   static void dproj(const DenseProjArgs& a, const ModParams& mp, cudaStream_t s) {
     dense_project_launch<L>(a, mp, s);
   }
-  static LOps make() { return LOps{pass, p2s, s2p, l2s, s2l, mont, zero, dproj}; }
+  static void addm(const AddModArgs& a, const ModParams& mp, cudaStream_t s) {
+    if (a.n) add_mod_kernel<L><<<blocks_for(a.n, 128), 128, 0, s>>>(a, mp);
+  }
+  static void rrows(const uint32_t* v, const int64_t* r, int m, uint32_t* o, cudaStream_t s) {
+    if (m) read_rows_kernel<L><<<blocks_for(m, 128), 128, 0, s>>>(v, r, m, o);
+  }
+  static LOps make() { return LOps{pass, p2s, s2p, l2s, s2l, mont, zero, dproj, addm, rrows}; }
 };
 
 template <int L, int LMIN>
