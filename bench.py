@@ -235,8 +235,15 @@ def run_grid(args, cfg, rank, world, local, dist, log):
     from paper_1402_3661_b200.corpus import _random_residue_limbs
     from paper_1402_3661_b200.grid import B200Grid, GridComm
     if dist is None:
-        tdist.init_process_group("nccl" if torch.cuda.is_available() else "gloo",
-                                 init_method="tcp://127.0.0.1:29533", rank=0, world_size=1)
+        import datetime
+        import socket
+        if "MASTER_ADDR" not in os.environ:  # plain `python bench.py`: a private 1-rank group
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
+                              RANK="0", WORLD_SIZE="1")
+            sk.close()
+        tdist.init_process_group("nccl", timeout=datetime.timedelta(seconds=300))
     g = GridSpec.parse(args.grid) if args.grid else GridSpec(world, 1)
     A, _, mod = build_matrix(cfg, log)
     t = time.time()
@@ -312,7 +319,9 @@ def main():
         import torch.distributed as dist
         if args.impl == "ours":
             torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        import datetime
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo",
+                                timeout=datetime.timedelta(seconds=600))
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         if dist is not None:

@@ -123,6 +123,10 @@ struct sld_ctx {
   ModParams mp;
   size_t l2_bytes = 0;
   int sms = 0;
+  void* hstage = nullptr;  // pinned host staging (limb format)
+  size_t hstage_bytes = 0;
+  void* dstage = nullptr;  // device staging (limb format)
+  size_t dstage_bytes = 0;
 };
 
 struct sld_vec {
@@ -149,7 +153,7 @@ struct sld_mat {
   int64_t n_pm = 0, n_small = 0, n_full = 0, pad_entries = 0;
   int64_t max_deg = 0;
   size_t dev_bytes = 0;
-  int policy = 6;  // L2 policy bits (SpmvArgs::policy); env SLD_POLICY overrides
+  int policy = 7;  // L2 policy bits (SpmvArgs::policy), measured best; env SLD_POLICY overrides
   // device
   SliceInfo* slices = nullptr;  // [npass][nslices]
   uint4* pm_idx = nullptr;
@@ -277,6 +281,8 @@ extern "C" int sld_ctx_destroy(sld_ctx* c) {
   if (!c) return SLD_OK;
   cudaSetDevice(c->dev);
   if (c->own) cudaStreamDestroy(c->own);
+  if (c->hstage) cudaFreeHost(c->hstage);
+  if (c->dstage) cudaFree(c->dstage);
   delete c;
   return SLD_OK;
 }
@@ -349,39 +355,125 @@ extern "C" int sld_vec_device_ptr(sld_vec* v, uint64_t* ptr, int64_t* stride) {
   return SLD_OK;
 }
 
-static int upload_planes_dev(sld_vec* v, const uint64_t* planes, int64_t n, int P, uint64_t** stage,
-                             size_t* stage_bytes) {
-  sld_ctx* c = v->ctx;
-  const size_t bytes = (size_t)n * P * 8;
-  if (*stage_bytes < bytes) {
-    if (*stage) cudaFree(*stage);
-    *stage = nullptr;
-    *stage_bytes = 0;
-    CU(cudaMalloc(stage, bytes ? bytes : 8));
-    *stage_bytes = bytes;
+// ---- host <-> device transfers: threaded repack into pinned staging, DMA
+// in chunks so the CPU repack of chunk k+1 overlaps the copy of chunk k.
+
+static int ensure_stage(sld_ctx* c, size_t bytes) {
+  if (c->hstage_bytes < bytes) {
+    if (c->hstage) cudaFreeHost(c->hstage);
+    c->hstage = nullptr;
+    c->hstage_bytes = 0;
+    CU(cudaHostAlloc(&c->hstage, bytes, cudaHostAllocPortable));
+    c->hstage_bytes = bytes;
   }
-  if (bytes) CU(cudaMemcpyAsync(*stage, planes, bytes, cudaMemcpyHostToDevice, c->stream));
-  ops(c->L).planes_to_slots(*stage, P, n, v->buf[v->cur], c->stream);
-  CU(cudaGetLastError());
+  if (c->dstage_bytes < bytes) {
+    if (c->dstage) cudaFree(c->dstage);
+    c->dstage = nullptr;
+    c->dstage_bytes = 0;
+    CU(cudaMalloc(&c->dstage, bytes));
+    c->dstage_bytes = bytes;
+  }
   return SLD_OK;
 }
 
-static int download_planes_dev(sld_vec* v, uint64_t* planes, int64_t n, int P, uint64_t** stage,
-                               size_t* stage_bytes) {
-  sld_ctx* c = v->ctx;
-  const size_t bytes = (size_t)n * P * 8;
-  if (*stage_bytes < bytes) {
-    if (*stage) cudaFree(*stage);
-    *stage = nullptr;
-    *stage_bytes = 0;
-    CU(cudaMalloc(stage, bytes ? bytes : 8));
-    *stage_bytes = bytes;
+template <typename F>
+static void host_par(int64_t n, F f) {
+  const int nt = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n < 65536 || nt == 1) {
+    f(0, n);
+    return;
   }
-  ops(c->L).slots_to_planes(v->buf[v->cur], n, P, *stage, c->stream);
+  std::vector<std::thread> th;
+  const int64_t chunk = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; t++) {
+    const int64_t lo = t * chunk, hi = std::min<int64_t>(n, lo + chunk);
+    if (lo < hi) th.emplace_back([=] { f(lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
+
+static constexpr int64_t XFER_CHUNK = 1 << 19;  // rows per DMA chunk
+
+// rows of planes (P 16-bit digits in uint64 cells) or limbs (L words) -> device slots
+static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs, int64_t n, int P) {
+  sld_ctx* c = v->ctx;
+  const int L = c->L;
+  const size_t bytes = (size_t)n * L * 4;
+  if (!n) return SLD_OK;
+  TRY(ensure_stage(c, bytes));
+  uint32_t* h = (uint32_t*)c->hstage;
+  uint32_t* d = (uint32_t*)c->dstage;
+  for (int64_t lo = 0; lo < n; lo += XFER_CHUNK) {
+    const int64_t hi = std::min(n, lo + XFER_CHUNK);
+    host_par(hi - lo, [&](int64_t a, int64_t b) {
+      for (int64_t r = lo + a; r < lo + b; r++) {
+        uint32_t* dst = h + (size_t)r * L;
+        if (planes) {
+          const uint64_t* src = planes + (size_t)r * P;
+          for (int j = 0; j < L; j++) {
+            const uint32_t d0 = 2 * j < P ? (uint32_t)(src[2 * j] & 0xFFFF) : 0u;
+            const uint32_t d1 = 2 * j + 1 < P ? (uint32_t)(src[2 * j + 1] & 0xFFFF) : 0u;
+            dst[j] = d0 | (d1 << 16);
+          }
+        } else {
+          memcpy(dst, limbs + (size_t)r * L, 4 * (size_t)L);
+        }
+      }
+    });
+    CU(cudaMemcpyAsync(d + (size_t)lo * L, h + (size_t)lo * L, (size_t)(hi - lo) * L * 4,
+                       cudaMemcpyHostToDevice, c->stream));
+  }
+  ops(L).limbs_to_slots(d, n, v->buf[v->cur], 0x80000000u, c->stream);
   CU(cudaGetLastError());
-  if (bytes) CU(cudaMemcpyAsync(planes, *stage, bytes, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return SLD_OK;
+}
+
+static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t n, int P) {
+  sld_ctx* c = v->ctx;
+  const int L = c->L;
+  const size_t bytes = (size_t)n * L * 4;
+  if (!n) return SLD_OK;
+  TRY(ensure_stage(c, bytes));
+  uint32_t* h = (uint32_t*)c->hstage;
+  uint32_t* d = (uint32_t*)c->dstage;
+  ops(L).slots_to_limbs(v->buf[v->cur], n, d, 0x80000000u, c->stream);
+  CU(cudaGetLastError());
+  std::vector<cudaEvent_t> ev;
+  for (int64_t lo = 0; lo < n; lo += XFER_CHUNK) {
+    const int64_t hi = std::min(n, lo + XFER_CHUNK);
+    CU(cudaMemcpyAsync(h + (size_t)lo * L, d + (size_t)lo * L, (size_t)(hi - lo) * L * 4,
+                       cudaMemcpyDeviceToHost, c->stream));
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CU(cudaEventRecord(e, c->stream));
+    ev.push_back(e);
+  }
+  int k = 0;
+  int rc = SLD_OK;
+  for (int64_t lo = 0; lo < n; lo += XFER_CHUNK, k++) {
+    const int64_t hi = std::min(n, lo + XFER_CHUNK);
+    cudaError_t e = cudaEventSynchronize(ev[k]);
+    if (e != cudaSuccess && rc == SLD_OK) rc = fail(SLD_E_CUDA, "download: %s", cudaGetErrorString(e));
+    if (rc != SLD_OK) continue;
+    host_par(hi - lo, [&](int64_t a, int64_t b) {
+      for (int64_t r = lo + a; r < lo + b; r++) {
+        const uint32_t* src = h + (size_t)r * L;
+        if (planes) {
+          uint64_t* dst = planes + (size_t)r * P;
+          for (int q = 0; q < P; q++) {
+            const int j = q >> 1;
+            const uint32_t w = j < L ? src[j] : 0u;
+            dst[q] = (q & 1) ? (w >> 16) : (w & 0xFFFF);
+          }
+        } else {
+          memcpy(limbs + (size_t)r * L, src, 4 * (size_t)L);
+        }
+      }
+    });
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  return rc;
 }
 
 static int check_P(const sld_ctx* c, int P) {
@@ -394,53 +486,26 @@ extern "C" int sld_vec_upload_planes(sld_vec* v, const uint64_t* planes, int64_t
   if (!v || n != v->n) return fail(SLD_E_ARG, "plane count mismatch");
   TRY(check_P(v->ctx, P));
   CU(cudaSetDevice(v->ctx->dev));
-  uint64_t* stage = nullptr;
-  size_t sb = 0;
-  int r = upload_planes_dev(v, planes, n, P, &stage, &sb);
-  cudaStreamSynchronize(v->ctx->stream);
-  if (stage) cudaFree(stage);
-  return r;
+  return upload_rows(v, planes, nullptr, n, P);
 }
 
 extern "C" int sld_vec_download_planes(sld_vec* v, uint64_t* planes, int64_t n, int P) {
   if (!v || n > v->n || n < 0) return fail(SLD_E_ARG, "plane count mismatch");
   TRY(check_P(v->ctx, P));
   CU(cudaSetDevice(v->ctx->dev));
-  uint64_t* stage = nullptr;
-  size_t sb = 0;
-  int r = download_planes_dev(v, planes, n, P, &stage, &sb);
-  if (stage) cudaFree(stage);
-  return r;
+  return download_rows(v, planes, nullptr, n, P);
 }
 
 extern "C" int sld_vec_upload_limbs(sld_vec* v, const uint32_t* limbs, int64_t n) {
   if (!v || n != v->n) return fail(SLD_E_ARG, "limb count mismatch");
-  sld_ctx* c = v->ctx;
-  CU(cudaSetDevice(c->dev));
-  uint32_t* d = nullptr;
-  const size_t bytes = (size_t)n * c->L * 4;
-  CU(cudaMalloc(&d, bytes ? bytes : 4));
-  if (bytes) CU(cudaMemcpyAsync(d, limbs, bytes, cudaMemcpyHostToDevice, c->stream));
-  ops(c->L).limbs_to_slots(d, n, v->buf[v->cur], 0x80000000u, c->stream);
-  cudaError_t e = cudaStreamSynchronize(c->stream);
-  cudaFree(d);
-  if (e != cudaSuccess) return fail(SLD_E_CUDA, "upload: %s", cudaGetErrorString(e));
-  return SLD_OK;
+  CU(cudaSetDevice(v->ctx->dev));
+  return upload_rows(v, nullptr, limbs, n, 0);
 }
 
 extern "C" int sld_vec_download_limbs(sld_vec* v, uint32_t* limbs, int64_t n) {
   if (!v || n > v->n || n < 0) return fail(SLD_E_ARG, "limb count mismatch");
-  sld_ctx* c = v->ctx;
-  CU(cudaSetDevice(c->dev));
-  uint32_t* d = nullptr;
-  const size_t bytes = (size_t)n * c->L * 4;
-  CU(cudaMalloc(&d, bytes ? bytes : 4));
-  ops(c->L).slots_to_limbs(v->buf[v->cur], n, d, 0x80000000u, c->stream);
-  if (bytes) CU(cudaMemcpyAsync(limbs, d, bytes, cudaMemcpyDeviceToHost, c->stream));
-  cudaError_t e = cudaStreamSynchronize(c->stream);
-  cudaFree(d);
-  if (e != cudaSuccess) return fail(SLD_E_CUDA, "download: %s", cudaGetErrorString(e));
-  return SLD_OK;
+  CU(cudaSetDevice(v->ctx->dev));
+  return download_rows(v, nullptr, limbs, n, 0);
 }
 
 extern "C" int sld_vec_read_rows(sld_vec* v, const int64_t* rows, int m, uint32_t* limbs) {
@@ -896,10 +961,10 @@ extern "C" int sld_spmv_planes(sld_mat* M, const uint64_t* in_planes, uint64_t* 
   CU(cudaSetDevice(c->dev));
   if (!M->tmp_in) TRY(sld_vec_create(c, M->total_cols, &M->tmp_in));
   if (!M->tmp_out) TRY(sld_vec_create(c, M->nrows, &M->tmp_out));
-  TRY(upload_planes_dev(M->tmp_in, in_planes, M->total_cols, P, &M->stage, &M->stage_bytes));
+  TRY(upload_rows(M->tmp_in, in_planes, nullptr, M->total_cols, P));
   launch_product(M, M->tmp_in->buf[0], M->tmp_out->buf[0], nullptr, 0, nullptr);
   CU(cudaGetLastError());
-  TRY(download_planes_dev(M->tmp_out, out_planes, M->nrows, P, &M->stage, &M->stage_bytes));
+  TRY(download_rows(M->tmp_out, out_planes, nullptr, M->nrows, P));
   return SLD_OK;
 }
 

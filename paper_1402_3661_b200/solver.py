@@ -154,7 +154,9 @@ class B200Multiplier:
         with self._lock:
             dm = self.dm
             P = v_planes.shape[1]
-            vec = dm.vector()
+            if getattr(self, "_vec", None) is None:
+                self._vec = dm.vector()  # kept: device iterate + its ping-pong twin
+            vec = self._vec
             vec.upload_planes(v_planes)
             if isinstance(xblock, UnitRows):
                 terms = dm.krylov_unit(vec, xblock.rows, steps)
@@ -164,7 +166,6 @@ class B200Multiplier:
             else:
                 raise TypeError(f"unsupported projection block {type(xblock).__name__}")
             v_out = vec.download_planes(P)
-            vec.close()
         self.count += int(steps)
         m = terms.shape[1]
         flat = limbs_to_ints(terms.reshape(-1, terms.shape[2])) if terms.size else []
