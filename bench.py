@@ -52,8 +52,12 @@ L2_GATHER_PEAK_GBS = 9200.0  # measured random 32-byte L2 gather rate, profiles/
 
 
 def dist_env():
-    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
-            int(os.environ.get("LOCAL_RANK", "0")))
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = int(os.environ.get("SLD_BENCH_NDEV", "0"))
+    if ndev:  # test hook: fold more ranks than GPUs onto the visible devices
+        local %= ndev
+    return rank, world, local
 
 
 def measured_peaks():
@@ -290,6 +294,14 @@ def run_grid(args, cfg, rank, world, local, dist, log):
         print(json.dumps(line), flush=True)
 
 
+def max_over_ranks(dist, x, local):
+    import torch
+    dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def config_block(name, cfg, A, mod, world):
     return {"workload": f"{name}: {cfg['desc']}", "N": A.nrows, "nnz": int(len(A.col_idx)),
             "ell_bits": mod.bit_length, "gamma": cfg["gamma"], "bp": list(cfg["bp"]),
@@ -315,13 +327,15 @@ def main():
     rank, world, local = dist_env()
     dist = None
     if world > 1:
+        import datetime
         import torch
         import torch.distributed as dist
-        if args.impl == "ours":
+        backend = os.environ.get("SLD_BENCH_BACKEND") or ("nccl" if args.impl == "ours" else "gloo")
+        kw = {}
+        if backend == "nccl":
             torch.cuda.set_device(local)
-        import datetime
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo",
-                                timeout=datetime.timedelta(seconds=600))
+            kw["device_id"] = torch.device(f"cuda:{local}")
+        dist.init_process_group(backend, timeout=datetime.timedelta(seconds=600), **kw)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         if dist is not None:
@@ -364,10 +378,8 @@ def main():
     if dist is not None:
         import torch
         torch.cuda.synchronize()
-        t_all = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+        total_ms = max_over_ranks(dist, total_ms, local)
         dist.barrier()
-        total_ms = float(t_all.item())
     steps_even = 2 * ((args.steps + 1) // 2)  # the bench graph replays product pairs
     ms_per_step = total_ms / steps_even
     value = world * steps_even / (total_ms / 1e3)
@@ -388,9 +400,7 @@ def main():
         t_e2e = time.perf_counter() - t0
     if dist is not None:
         import torch
-        te = torch.tensor([t_e2e], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        t_e2e = float(te.item())
+        t_e2e = max_over_ranks(dist, t_e2e, local)
     e2e_value = world * e2e_steps / t_e2e
     h2d = y_planes.nbytes + 8 * bp_m
     d2h = e2e_steps * bp_m * 4 * L + v_out.nbytes

@@ -127,6 +127,7 @@ struct sld_ctx {
   size_t hstage_bytes = 0;
   void* dstage = nullptr;  // device staging (limb format)
   size_t dstage_bytes = 0;
+  size_t apw_max = 0;      // max access-policy window bytes (0: unsupported)
 };
 
 struct sld_vec {
@@ -154,6 +155,8 @@ struct sld_mat {
   int64_t max_deg = 0;
   size_t dev_bytes = 0;
   int policy = 7;  // L2 policy bits (SpmvArgs::policy), measured best; env SLD_POLICY overrides
+  int apw = 0;       // persisting L2 access-policy window over the gathered stripe (env SLD_APW)
+  float apw_ratio = 1.0f;
   // device
   SliceInfo* slices = nullptr;  // [npass][nslices]
   uint4* pm_idx = nullptr;
@@ -271,6 +274,9 @@ extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_
   CU(cudaGetDeviceProperties(&pr, device));
   c->l2_bytes = pr.l2CacheSize;
   c->sms = pr.multiProcessorCount;
+  c->apw_max = pr.accessPolicyMaxWindowSize > 0 ? (size_t)pr.accessPolicyMaxWindowSize : 0;
+  if (getenv("SLD_APW") && pr.persistingL2CacheMaxSize > 0)
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pr.persistingL2CacheMaxSize);
   CU(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
   *out = c.release();
@@ -875,6 +881,8 @@ extern "C" int sld_mat_create(sld_ctx* ctx, int64_t nrows, int64_t ncols, const 
   M->total_cols = ncols + n_dense;
   M->nnz = nnz;
   if (const char* pe = getenv("SLD_POLICY")) M->policy = atoi(pe);
+  if (const char* pe = getenv("SLD_APW")) M->apw = atoi(pe);
+  if (const char* pe = getenv("SLD_APW_RATIO")) M->apw_ratio = (float)atof(pe);
   int r = mat_build(M, row_ptr, col_idx, tags, small_vals, n_full, full_pos, full_limbs, dense_limbs,
                     max_stripe_cols);
   if (r != SLD_OK) {
@@ -936,7 +944,26 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
   for (int p = 0; p < M->npass; p++) {
     a.slices = M->slices + (size_t)p * M->nslices;
     a.lane_k4 = M->lane_k4 + (size_t)p * M->nslices * 32;
+    if (M->apw && c->apw_max) {
+      // persisting L2 window over the stripe this pass gathers from
+      const int64_t lo = (int64_t)p * M->stripe_cols;
+      const int64_t hi = std::min<int64_t>(M->total_cols + 1, lo + M->stripe_cols);
+      cudaStreamAttrValue v;
+      memset(&v, 0, sizeof(v));
+      v.accessPolicyWindow.base_ptr = (void*)(x + (size_t)lo * c->SW);
+      v.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)(hi - lo) * c->SW * 4, c->apw_max);
+      v.accessPolicyWindow.hitRatio = M->apw_ratio;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    }
     o.pass(p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
+  }
+  if (M->apw && c->apw_max) {
+    cudaStreamAttrValue v;
+    memset(&v, 0, sizeof(v));
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
   }
 }
 

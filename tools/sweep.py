@@ -20,13 +20,19 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--policies", default="6")
     ap.add_argument("--stripes", default="0")
+    ap.add_argument("--apw", default="0", help="comma list of SLD_APW_RATIO values; 0 = off")
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
     y = _random_residue_limbs(np.random.default_rng(5), A.total_cols, mod)
     for sc in [int(x) for x in a.stripes.split(",")]:
-        for pol in [int(x) for x in a.policies.split(",")]:
+        for pol, apw in [(int(x), float(y)) for x in a.policies.split(",") for y in a.apw.split(",")]:
             os.environ["SLD_POLICY"] = str(pol)
+            if apw > 0:
+                os.environ["SLD_APW"] = "1"
+                os.environ["SLD_APW_RATIO"] = str(apw)
+            else:
+                os.environ.pop("SLD_APW", None)
             dm = DeviceMatrix(A, stripe_cols=sc)
             v = dm.vector()
             v.upload_limbs(y)
@@ -37,7 +43,7 @@ def main():
             import subprocess
             clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.mem,power.draw,temperature.gpu",
                                   "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
-            print(f"{a.config} stripes={dm.info()['stripes']} policy={pol}: {per:.4f} ms/product  [{clk}]",
+            print(f"{a.config} stripes={dm.info()['stripes']} policy={pol} apw={apw}: {per:.4f} ms/product  [{clk}]",
                   flush=True)
             v.close()
             dm.close()
