@@ -118,6 +118,18 @@ int sld_vec_device_ptr(sld_vec *v, uint64_t *ptr, int64_t *stride_words);
  */
 int sld_add_mod(sld_ctx *ctx, const uint64_t *src_ptrs, int k, uint64_t dst_ptr, int64_t n);
 
+/*
+ * dst = acc + sum_j coeffs_j * y_j (mod l) over n residues in the slot
+ * format (raw device pointers; acc_ptr may be 0; k <= 64 canonical
+ * coefficients as k x L limbs).  The Horner combination of Mksol
+ * (solver.py:522-536: planes_scalar_mul_mod + planes_add_mod).
+ */
+int sld_lincomb(sld_ctx *ctx, const uint64_t *y_ptrs, const uint32_t *coeffs, int k,
+                uint64_t acc_ptr, uint64_t dst_ptr, int64_t n);
+
+/* *out = 1 if any residue of v is non-zero (np.any(planes), solver.py:545). */
+int sld_vec_nonzero(sld_vec *v, int *out);
+
 /* Read m residues (rows[t] of the vector) as canonical limbs (m x L). */
 int sld_vec_read_rows(sld_vec *v, const int64_t *rows, int m, uint32_t *limbs);
 

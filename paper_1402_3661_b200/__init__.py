@@ -16,6 +16,7 @@ from .spmatrix import DeviceKernel, SparseMatrix, classify, spmv_planes, spmv_se
 from .solver import (
     B200Multiplier, BlockingParams, BlockSequence, DenseRows, SequentialMultiplier, UnitRows,
     draw_blocks, krylov_block, krylov_column, krylov_length, krylov_scalar,
+    GeneratorFailure, KernelVector, SolverFailure, mksol_block, mksol_scalar, verify_kernel,
 )
 
 __version__ = "0.1.0"

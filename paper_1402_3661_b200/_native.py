@@ -24,7 +24,7 @@ SLD_E_NCCL = -4
 EXPORTS = [
     "sld_version", "sld_last_error", "sld_device_count",
     "sld_ctx_create", "sld_ctx_destroy", "sld_ctx_sync", "sld_ctx_set_stream", "sld_add_mod",
-    "sld_vec_read_rows",
+    "sld_vec_read_rows", "sld_lincomb", "sld_vec_nonzero",
     "sld_mat_create", "sld_mat_destroy", "sld_mat_info",
     "sld_vec_create", "sld_vec_destroy", "sld_vec_upload_planes", "sld_vec_download_planes",
     "sld_vec_upload_limbs", "sld_vec_download_limbs", "sld_vec_device_ptr",
@@ -73,6 +73,8 @@ def load(build_if_missing=False):
             "sld_ctx_set_stream": ([vp, ctypes.c_uint64], i32),
             "sld_add_mod": ([vp, vp, i32, ctypes.c_uint64, i64], i32),
             "sld_vec_read_rows": ([vp, vp, i32, vp], i32),
+            "sld_lincomb": ([vp, vp, vp, i32, ctypes.c_uint64, ctypes.c_uint64, i64], i32),
+            "sld_vec_nonzero": ([vp, vp], i32),
             "sld_mat_create": ([vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, i32, vp, i64, pp], i32),
             "sld_mat_destroy": ([vp], i32),
             "sld_mat_info": ([vp, vp], i32),

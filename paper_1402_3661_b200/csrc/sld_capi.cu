@@ -514,6 +514,52 @@ extern "C" int sld_vec_download_limbs(sld_vec* v, uint32_t* limbs, int64_t n) {
   return download_rows(v, nullptr, limbs, n, 0);
 }
 
+extern "C" int sld_lincomb(sld_ctx* c, const uint64_t* y_ptrs, const uint32_t* coeffs, int k,
+                           uint64_t acc_ptr, uint64_t dst_ptr, int64_t n) {
+  if (!c || k < 0 || k > 64 || n < 0 || !dst_ptr || (k && (!y_ptrs || !coeffs)))
+    return fail(SLD_E_ARG, "bad lincomb arguments");
+  CU(cudaSetDevice(c->dev));
+  LinCombArgs a;
+  memset(&a, 0, sizeof(a));
+  uint32_t* dc = nullptr;
+  if (k) {
+    std::vector<uint32_t> h((size_t)k * c->SW, 0);
+    for (int j = 0; j < k; j++)
+      for (int i = 0; i < c->L; i++) h[(size_t)j * c->SW + i] = coeffs[(size_t)j * c->L + i];
+    CU(cudaMalloc(&dc, h.size() * 4));
+    CU(cudaMemcpyAsync(dc, h.data(), h.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    ops(c->L).to_mont(dc, k, c->mp, c->stream);
+  }
+  for (int j = 0; j < k; j++) a.y[j] = (const uint32_t*)(uintptr_t)y_ptrs[j];
+  a.coef = dc;
+  a.acc = (const uint32_t*)(uintptr_t)acc_ptr;
+  a.dst = (uint32_t*)(uintptr_t)dst_ptr;
+  a.k = k;
+  a.n = n;
+  ops(c->L).lincomb(a, c->mp, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (dc) cudaFree(dc);
+  if (e != cudaSuccess) return fail(SLD_E_CUDA, "lincomb: %s", cudaGetErrorString(e));
+  return SLD_OK;
+}
+
+extern "C" int sld_vec_nonzero(sld_vec* v, int* out) {
+  if (!v || !out) return fail(SLD_E_ARG, "null argument");
+  sld_ctx* c = v->ctx;
+  CU(cudaSetDevice(c->dev));
+  int* d = nullptr;
+  CU(cudaMalloc(&d, 4));
+  cudaMemsetAsync(d, 0, 4, c->stream);
+  ops(c->L).nonzero(v->buf[v->cur], v->n, d, c->stream);
+  int h = 0;
+  cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(SLD_E_CUDA, "nonzero: %s", cudaGetErrorString(e));
+  *out = h;
+  return SLD_OK;
+}
+
 extern "C" int sld_vec_read_rows(sld_vec* v, const int64_t* rows, int m, uint32_t* limbs) {
   if (!v || m < 0 || (m && (!rows || !limbs))) return fail(SLD_E_ARG, "bad read_rows arguments");
   for (int t = 0; t < m; t++)

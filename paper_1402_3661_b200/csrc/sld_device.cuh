@@ -508,6 +508,62 @@ __global__ void add_mod_kernel(const AddModArgs a, const ModParams mp) {
   store_slot<SW>(a.dst + (size_t)i * SW, o);
 }
 
+// dst = acc + sum_j c_j y_j mod ell (Mksol's Horner combination,
+// solver.py:522-536): c_j in Montgomery form (c R mod ell) so one CIOS
+// product gives c_j y_j mod ell < ell; acc / y_j / dst in biased slots.
+struct LinCombArgs {
+  const uint32_t* y[64];
+  const uint32_t* coef;  // k coefficients, SW words each, Montgomery form
+  const uint32_t* acc;   // optional
+  uint32_t* dst;
+  int k;
+  int64_t n;
+};
+
+template <int L>
+__global__ void lincomb_kernel(const LinCombArgs a, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  int64_t acc[L + 1];
+#pragma unroll
+  for (int j = 0; j <= L; j++) acc[j] = 0;
+  if (a.acc) {
+#pragma unroll
+    for (int j = 0; j < L; j++) acc[j] += a.acc[(size_t)i * SW + j] ^ 0x80000000u;
+  }
+  for (int s = 0; s < a.k; s++) {
+    uint32_t u[L], c[L], r[L];
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+      u[j] = a.y[s][(size_t)i * SW + j] ^ 0x80000000u;
+      c[j] = a.coef[(size_t)s * SW + j];
+    }
+    montmul<L>(c, u, mp, r);
+#pragma unroll
+    for (int j = 0; j < L; j++) acc[j] += r[j];
+  }
+  uint32_t R[L];
+  finalize<L>(acc, 0, mp, R);
+  uint32_t o[SW];
+#pragma unroll
+  for (int j = 0; j < SW; j++) o[j] = j < L ? (R[j] ^ 0x80000000u) : 0u;
+  store_slot<SW>(a.dst + (size_t)i * SW, o);
+}
+
+// *flag |= 1 if any of the n residues is non-zero
+template <int L>
+__global__ void nonzero_kernel(const uint32_t* __restrict__ v, int64_t n, int* flag) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool nz = false;
+  if (i < n) {
+#pragma unroll
+    for (int j = 0; j < L; j++) nz |= (v[(size_t)i * SW + j] ^ 0x80000000u) != 0u;
+  }
+  if (__any_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 // out[t] = canonical limbs of slot rows[t]
 template <int L>
 __global__ void read_rows_kernel(const uint32_t* __restrict__ v, const int64_t* __restrict__ rows, int m,

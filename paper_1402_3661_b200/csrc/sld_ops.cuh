@@ -21,6 +21,8 @@ struct LOps {
   void (*dense_proj)(const DenseProjArgs&, const ModParams&, cudaStream_t);
   void (*add_mod)(const AddModArgs&, const ModParams&, cudaStream_t);
   void (*read_rows)(const uint32_t*, const int64_t*, int, uint32_t*, cudaStream_t);
+  void (*lincomb)(const LinCombArgs&, const ModParams&, cudaStream_t);
+  void (*nonzero)(const uint32_t*, int64_t, int*, cudaStream_t);
 };
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -61,7 +63,13 @@ struct Ops {
   static void rrows(const uint32_t* v, const int64_t* r, int m, uint32_t* o, cudaStream_t s) {
     if (m) read_rows_kernel<L><<<blocks_for(m, 128), 128, 0, s>>>(v, r, m, o);
   }
-  static LOps make() { return LOps{pass, p2s, s2p, l2s, s2l, mont, zero, dproj, addm, rrows}; }
+  static void lcomb(const LinCombArgs& a, const ModParams& mp, cudaStream_t s) {
+    if (a.n) lincomb_kernel<L><<<blocks_for(a.n, 128), 128, 0, s>>>(a, mp);
+  }
+  static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
+    if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);
+  }
+  static LOps make() { return LOps{pass, p2s, s2p, l2s, s2l, mont, zero, dproj, addm, rrows, lcomb, nz}; }
 };
 
 template <int L, int LMIN>

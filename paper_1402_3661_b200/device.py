@@ -98,6 +98,18 @@ class DeviceVector:
     def handle(self):
         return self._h
 
+    @property
+    def ptr(self):
+        """Raw device pointer of the current buffer (slot format)."""
+        p, st = ctypes.c_uint64(), ctypes.c_int64()
+        N.check(N.load().sld_vec_device_ptr(self._h, ctypes.byref(p), ctypes.byref(st)))
+        return p.value
+
+    def nonzero(self) -> bool:
+        out = ctypes.c_int(0)
+        N.check(N.load().sld_vec_nonzero(self._h, ctypes.byref(out)))
+        return bool(out.value)
+
     def upload_planes(self, planes):
         p = np.ascontiguousarray(planes, dtype=np.uint64)
         if p.ndim != 2 or p.shape[0] != self.n:
@@ -130,6 +142,15 @@ class DeviceVector:
             self.close()
         except Exception:
             pass
+
+
+def lincomb(field: Field, ys, coeffs, dst: "DeviceVector", acc: "DeviceVector" = None):
+    """dst = acc + sum_j coeffs[j] * ys[j] mod l on the device."""
+    k = len(ys)
+    ptrs = np.array([y.ptr for y in ys], dtype=np.uint64)
+    cl = ints_to_limbs([int(c) for c in coeffs], field.L) if k else np.zeros((0, field.L), np.uint32)
+    N.check(N.load().sld_lincomb(field.handle, N.ptr(ptrs), N.ptr(cl), k,
+                                 acc.ptr if acc is not None else 0, dst.ptr, dst.n))
 
 
 class XBlock:

@@ -27,13 +27,37 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .device import DEFAULT_DEVICE, DeviceMatrix, XBlock
+from .device import DEFAULT_DEVICE, DeviceMatrix, XBlock, lincomb
 from .modring import (
     as_modulus, digit_count, ints_to_limbs, ints_to_planes, limbs_to_ints, limbs_to_planes,
     planes_to_ints, planes_to_limbs,
 )
 
 SAFETY_MARGIN = 32
+MAX_RESTARTS = 3
+
+
+class SolverFailure(RuntimeError):
+    """The candidate kernel vector degenerated to zero (solver.py:44-46)."""
+
+
+class GeneratorFailure(RuntimeError):
+    """No usable linear generator (solver.py:49-50)."""
+
+
+@dataclass
+class KernelVector:
+    w: list
+    verified: bool
+    horner_spmvs: int = 0
+    tail_spmvs: int = 0
+
+
+def _poly_degree(p) -> int:
+    for i in range(len(p) - 1, -1, -1):
+        if p[i]:
+            return i
+    return -1
 
 
 @dataclass(frozen=True)
@@ -173,6 +197,56 @@ class B200Multiplier:
         return out, v_out
 
 
+    def mksol(self, Y_planes, polys):
+        """Mksol on the device (solver.py:508-552): w = sum_j G_j(B) y_j by
+        one Horner chain (SpMV, then the fused combination kernel), then the
+        tail B^t w until zero.  Returns (w planes, verified, horner, tail)."""
+        with self._lock:
+            dm = self.dm
+            P = Y_planes[0].shape[1]
+            trimmed = [list(p)[: _poly_degree(p) + 1] for p in polys]
+            if not any(_poly_degree(p) >= 0 for p in trimmed):
+                raise GeneratorFailure("all-zero generators")
+            val = min(next((i for i, c in enumerate(p) if c), len(p)) for p in trimmed)
+            G = [p[val:] if len(p) > val else [0] for p in trimmed]
+            dmax = max(_poly_degree(p) for p in G)
+            ys = []
+            for yp in Y_planes:
+                y = dm.vector()
+                y.upload_planes(yp)
+                ys.append(y)
+            w, t = dm.vector(), dm.vector()
+
+            def combo(i, acc, dst):
+                sel = [(ys[j], p[i]) for j, p in enumerate(G) if i <= _poly_degree(p) and p[i]]
+                for k0 in range(0, max(1, len(sel)), 64):
+                    part = sel[k0:k0 + 64]
+                    lincomb(dm.field, [y for y, _ in part], [c for _, c in part], dst,
+                            acc if k0 == 0 else dst)
+
+            combo(dmax, None, w)
+            horner = 0
+            for i in range(dmax - 1, -1, -1):
+                dm.spmv(w, t)
+                horner += 1
+                combo(i, t, w)
+            tail = 0
+            dm.spmv(w, t)
+            while t.nonzero() and tail < val:
+                w, t = t, w
+                tail += 1
+                dm.spmv(w, t)
+            verified = (not t.nonzero()) and w.nonzero()
+            w_nonzero = w.nonzero()
+            w_planes = w.download_planes(P)
+            for v in ys + [w, t]:
+                v.close()
+        self.count += horner + tail + 1
+        if not w_nonzero:
+            raise SolverFailure("kernel candidate degenerated to zero")
+        return w_planes, verified, horner, tail
+
+
 # the reference's name for the default multiplier
 SequentialMultiplier = B200Multiplier
 
@@ -277,6 +351,75 @@ def krylov_scalar(A, x, y, count=None, mul=None) -> list:
     return [t[0] for t in terms]
 
 
+def _mksol_core(mul, Y_planes, polys, mod) -> KernelVector:
+    """w = sum_j G_j(B) y_j and its kernel check (solver.py:508-552).
+    Device-resident when the multiplier has `.mksol`; otherwise the
+    reference's loop over `mul.apply` with the combination in Python ints
+    (protocol compatibility for foreign multipliers, not a hot path)."""
+    if hasattr(mul, "mksol"):
+        w, verified, horner, tail = mul.mksol(Y_planes, polys)
+        kv = KernelVector(planes_to_ints(w), verified, horner_spmvs=horner, tail_spmvs=tail)
+        if not verified:
+            raise SolverFailure("candidate is not in the kernel after the tail")
+        return kv
+    ell = as_modulus(mod).ell
+    trimmed = [list(p)[: _poly_degree(p) + 1] for p in polys]
+    if not any(_poly_degree(p) >= 0 for p in trimmed):
+        raise GeneratorFailure("all-zero generators")
+    val = min(next((i for i, c in enumerate(p) if c), len(p)) for p in trimmed)
+    G = [p[val:] if len(p) > val else [0] for p in trimmed]
+    dmax = max(_poly_degree(p) for p in G)
+    width = Y_planes[0].shape[1]
+    Yi = [planes_to_ints(y) for y in Y_planes]
+
+    def combo(i, base=None):
+        acc = list(base) if base is not None else [0] * len(Yi[0])
+        for j, p in enumerate(G):
+            if i <= _poly_degree(p) and p[i]:
+                acc = [(a + p[i] * b) % ell for a, b in zip(acc, Yi[j])]
+        return acc
+
+    w = combo(dmax)
+    horner = 0
+    for i in range(dmax - 1, -1, -1):
+        w = combo(i, planes_to_ints(mul.apply(ints_to_planes(w, width))))
+        horner += 1
+    tail = 0
+    nxt = planes_to_ints(mul.apply(ints_to_planes(w, width)))
+    while any(nxt) and tail < val:
+        w = nxt
+        tail += 1
+        nxt = planes_to_ints(mul.apply(ints_to_planes(w, width)))
+    verified = not any(nxt) and any(w)
+    if not any(w):
+        raise SolverFailure("kernel candidate degenerated to zero")
+    kv = KernelVector(w, verified, horner_spmvs=horner, tail_spmvs=tail)
+    if not verified:
+        raise SolverFailure("candidate is not in the kernel after the tail")
+    return kv
+
+
+def mksol_scalar(A, y, F, mul=None) -> KernelVector:
+    if mul is None:
+        mul = B200Multiplier(A)
+    return _mksol_core(mul, [_as_planes(y, mul.mod)], [F], mul.mod)
+
+
+def mksol_block(A, Y, G, mul=None) -> KernelVector:
+    """G: Generators-like (`.polys`, one polynomial per y column)."""
+    if mul is None:
+        mul = B200Multiplier(A)
+    return _mksol_core(mul, [_as_planes(y, mul.mod) for y in Y], list(G.polys), mul.mod)
+
+
+def verify_kernel(A, w) -> bool:
+    """True iff A w = 0 and w != 0 (solver.py:568-573)."""
+    from .spmatrix import spmv_sequential
+    if not any(w):
+        return False
+    return not any(spmv_sequential(A, w))
+
+
 def draw_blocks(mod, size: int, bp, rng, x_mode="unit", forced_zero=()):
     """Random Y block and projection block (solver.py:578-596): the same
     draws in the same order, so seeds give the reference's blocks."""
@@ -298,6 +441,8 @@ def draw_blocks(mod, size: int, bp, rng, x_mode="unit", forced_zero=()):
 
 
 __all__ = [
+    "KernelVector", "SolverFailure", "GeneratorFailure", "mksol_block", "mksol_scalar",
+    "verify_kernel", "MAX_RESTARTS",
     "BlockingParams", "BlockSequence", "B200Multiplier", "SequentialMultiplier", "UnitRows",
     "DenseRows", "krylov_column", "krylov_block", "krylov_scalar", "krylov_length",
     "draw_blocks", "SAFETY_MARGIN", "planes_to_limbs", "limbs_to_planes",

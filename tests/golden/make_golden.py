@@ -42,7 +42,8 @@ from sldlag.corpus import CorpusProfile, generate  # noqa: E402
 from sldlag.gridmv import Grid, run_iterations  # noqa: E402
 from sldlag.modring import PrimeModulus  # noqa: E402
 from sldlag.solver import (  # noqa: E402
-    BlockingParams, DenseRows, UnitRows, draw_blocks, krylov_block,
+    BlockingParams, DenseRows, SolverFailure, UnitRows, berlekamp_massey, block_lingen,
+    draw_blocks, krylov_block, krylov_length, krylov_scalar, mksol_block, mksol_scalar,
 )
 from sldlag.spmatrix import SparseMatrix, spmv_sequential  # noqa: E402
 from test_spmatrix import random_matrix  # noqa: E402  (reference test helper)
@@ -245,12 +246,58 @@ def gen_grid_cases():
     return out
 
 
+def gen_mksol_cases():
+    """Mksol (solver.py:508-565) on generators from the reference's own
+    Krylov + Lingen: the kernel vector w, Horner/tail SpMV counts."""
+    out = {}
+    idx = 0
+    for ell, n, gamma, seed, bp in [
+        (2**61 - 1, 80, 6, 42, (2, 4)), (2**200 - 75, 90, 6, 7, (2, 4)),
+        (cli.random_prime(160, np.random.default_rng(1)).ell, 120, 8, 3, (3, 6)),
+        (2**61 - 1, 50, 5, 4, (1, 1)), (1009, 60, 5, 40, (2, 4)),
+    ]:
+        mod = PrimeModulus(ell)
+        A = generate(CorpusProfile(n=n, gamma=gamma, seed=seed), mod)
+        rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(0,)))
+        bpp = BlockingParams(*bp)
+        if bp == (1, 1):
+            x = mod.random_residues(rng, n)
+            y = mod.random_residues(rng, n)
+            F = berlekamp_massey(krylov_scalar(A, x, y), mod)
+            polys, Y = [F], [y]
+            try:
+                kv = mksol_scalar(A, y, F)
+            except SolverFailure:
+                continue
+        else:
+            X, Y = draw_blocks(mod, n, bpp, rng, "unit")
+            seq = krylov_block(A, X, Y, krylov_length(n, bpp))
+            polys = block_lingen(seq, bpp, n, mod, rng).polys
+            try:
+                kv = mksol_block(A, Y, type("G", (), {"polys": polys})())
+            except SolverFailure:
+                continue
+        pre = f"m{idx}_"
+        out.update(matrix_arrays(pre, A))
+        bw = mod.byte_width
+        out[pre + "Y"] = np.stack([res_bytes(y, bw) for y in Y])
+        dmax = max(len(pl) for pl in polys)
+        out[pre + "polys"] = np.stack([res_bytes(list(pl) + [0] * (dmax - len(pl)), bw) for pl in polys])
+        out[pre + "plen"] = np.array([len(pl) for pl in polys], dtype=np.int64)
+        out[pre + "w"] = res_bytes(kv.w, bw)
+        out[pre + "counts"] = np.array([kv.horner_spmvs, kv.tail_spmvs, int(kv.verified)], dtype=np.int64)
+        idx += 1
+    out["ncases"] = np.array(idx)
+    return out
+
+
 def main():
     jobs = {
         "spmv_cases.npz": gen_spmv_cases,
         "krylov_cases.npz": gen_krylov_cases,
         "grid_cases.npz": gen_grid_cases,
         "cfg1.npz": gen_cfg1,
+        "mksol_cases.npz": gen_mksol_cases,
     }
     only = sys.argv[1:]
     manifest = []
@@ -264,9 +311,18 @@ def main():
         h = hashlib.sha256(open(path, "rb").read()).hexdigest()
         manifest.append(f"{h}  {name}")
         print(name, os.path.getsize(path), "bytes")
-    if not only:
-        with open(os.path.join(HERE, "SHA256SUMS"), "w") as f:
-            f.write("\n".join(manifest) + "\n")
+    # refresh the manifest entries that were regenerated
+    path = os.path.join(HERE, "SHA256SUMS")
+    old = {}
+    if os.path.exists(path):
+        for line in open(path):
+            h, name = line.split()
+            old[name] = h
+    for line in manifest:
+        h, name = line.split()
+        old[name] = h
+    with open(path, "w") as f:
+        f.write("".join(f"{h}  {name}\n" for name, h in sorted(old.items())))
 
 
 if __name__ == "__main__":

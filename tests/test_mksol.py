@@ -1,0 +1,83 @@
+"""Mksol (solver.py:508-565) -- the f1 'next' row: the device Horner chain
+reproduces the reference's kernel vectors on generators from the
+reference's own Krylov + Lingen (tests/golden/mksol_cases.npz)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import fixture_sparse, to_oracle
+from paper_1402_3661_b200 import (
+    B200Multiplier, PrimeModulus, SolverFailure, SparseMatrix, mksol_block, mksol_scalar,
+    verify_kernel,
+)
+from paper_1402_3661_b200.modring import digit_count, ints_to_planes, planes_to_ints
+from paper_1402_3661_b200.solver import _mksol_core
+
+
+def _cases():
+    z = O.load_golden("mksol_cases.npz")
+    out = []
+    for i in range(int(z["ncases"])):
+        p = f"m{i}_"
+        A = fixture_sparse(z, p)
+        Y = [O.bytes_to_ints(y) for y in z[p + "Y"]]
+        polys = [O.bytes_to_ints(pl)[:n] for pl, n in zip(z[p + "polys"], z[p + "plen"])]
+        out.append((A, Y, polys, O.bytes_to_ints(z[p + "w"]), [int(x) for x in z[p + "counts"]]))
+    return out
+
+
+class _OracleMultiplier:
+    """TEST INFRASTRUCTURE: the multiplier protocol over the CPU oracle."""
+
+    def __init__(self, A):
+        self.orc, self.size, self.mod, self.count = to_oracle(A), A.nrows, A.mod, 0
+
+    def apply(self, planes):
+        self.count += 1
+        u = O.ints_to_limbs(planes_to_ints(planes), self.mod.limbs)
+        return ints_to_planes(O.limbs_to_ints(self.orc.spmv_limbs(u)), planes.shape[1])
+
+
+def test_generic_mksol_path_matches_reference_on_cpu():
+    for A, Y, polys, w, (horner, tail, ver) in _cases():
+        mul = _OracleMultiplier(A)
+        P = digit_count(A.mod.ell)
+        kv = _mksol_core(mul, [ints_to_planes(y, P) for y in Y], polys, A.mod)
+        assert kv.w == w and kv.horner_spmvs == horner and kv.tail_spmvs == tail and kv.verified
+
+
+@pytest.mark.gpu
+def test_device_mksol_matches_reference():
+    for A, Y, polys, w, (horner, tail, ver) in _cases():
+        mul = B200Multiplier(A)
+        kv = mksol_block(A, Y, type("G", (), {"polys": polys})(), mul=mul)
+        assert kv.w == w
+        assert (kv.horner_spmvs, kv.tail_spmvs, kv.verified) == (horner, tail, True)
+        assert mul.count == horner + tail + 1
+        assert verify_kernel(A, kv.w)
+
+
+@pytest.mark.gpu
+def test_mksol_tail_peels_common_factor():
+    # generators sharing X^2: w = G(B) y is peeled by B until B w = 0
+    mod = PrimeModulus(2**61 - 1)
+    # B: nilpotent shift  e_i -> e_{i+1}
+    n = 6
+    B = SparseMatrix.from_rows(mod, n, n, [[]] + [[(i - 1, 1)] for i in range(1, n)])
+    y = [0, 0, 0, 1, 0, 0]
+    # F(X) = X^3: G = 1, val = 3; w = y = e3, peeled to e5 (B e5 = 0)
+    kv = mksol_scalar(B, y, [0, 0, 0, 1])
+    assert (kv.horner_spmvs, kv.tail_spmvs) == (0, 2) and kv.verified
+    assert kv.w == [0, 0, 0, 0, 0, 1] and verify_kernel(B, kv.w)
+    # the generic (reference) loop agrees
+    P = digit_count(mod.ell)
+    kv2 = _mksol_core(_OracleMultiplier(B), [ints_to_planes(y, P)], [[0, 0, 0, 1]], mod)
+    assert kv2.w == kv.w and kv2.tail_spmvs == 2
+
+
+@pytest.mark.gpu
+def test_mksol_identity_fails_like_reference():
+    mod = PrimeModulus(2**61 - 1)
+    I = SparseMatrix.from_rows(mod, 4, 4, [[(i, 1)] for i in range(4)])
+    with pytest.raises(SolverFailure):
+        mksol_scalar(I, [1, 2, 3, 4], [mod.ell - 1, 1])  # X - 1 annihilates I: w = 0
