@@ -665,8 +665,17 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   // ---- stripes: keep the gathered column window L2-resident
   int64_t stripe = max_stripe_cols;
   if (stripe <= 0) {
-    const double budget = 0.50 * (double)c->l2_bytes;  // ~63 MB of the 126 MB L2 (measured best: 2 stripes at cfg3)
-    stripe = std::max<int64_t>(1, (int64_t)(budget / (SW * 4.0)));
+    // measured (tools/sweep.py): one pass while the gathered vector fits in
+    // ~80% of L2 (cfg2 21 MB, cfg5 96 MB); beyond that, stripes of <= 1/2 L2
+    // (cfg3: 2 x 58 MB) so each pass's working set stays L2-resident
+    const double vec_bytes = (double)(M->total_cols + 1) * SW * 4.0;
+    if (vec_bytes <= 0.80 * (double)c->l2_bytes) {
+      stripe = ncols;
+    } else {
+      const int64_t parts = (int64_t)std::ceil(vec_bytes / (0.5 * (double)c->l2_bytes));
+      stripe = (ncols + parts - 1) / parts;
+    }
+    stripe = std::max<int64_t>(1, stripe);
   }
   if (stripe >= ncols) stripe = std::max<int64_t>(ncols, 1);
   const int npass = (int)std::max<int64_t>(1, (ncols + stripe - 1) / stripe);
@@ -1230,30 +1239,37 @@ extern "C" int sld_bench_spmv(sld_mat* M, sld_vec* v, int64_t steps, int warmup,
   sld_ctx* c = M->ctx;
   CU(cudaSetDevice(c->dev));
   TRY(vec_alloc_buf(v, v->cur ^ 1));
-  // graph of 2 products (returns to the same buffer)
-  cudaGraph_t g;
-  cudaGraphExec_t ge;
-  CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  launch_product(M, v->buf[v->cur], v->buf[v->cur ^ 1], nullptr, 0, nullptr);
-  launch_product(M, v->buf[v->cur ^ 1], v->buf[v->cur], nullptr, 0, nullptr);
-  CU(cudaStreamEndCapture(c->stream, &g));
-  CU(cudaGraphInstantiate(&ge, g, 0));
-  CU(cudaGraphDestroy(g));
-  for (int w = 0; w < (warmup + 1) / 2; w++) CU(cudaGraphLaunch(ge, c->stream));
+  // graphs of 2 and 32 products (an even count returns to the same buffer);
+  // the long graph amortises launch latency for small matrices
+  cudaGraphExec_t ge2 = nullptr, ge32 = nullptr;
+  for (int reps : {1, 16}) {
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int r = 0; r < reps; r++) {
+      launch_product(M, v->buf[v->cur], v->buf[v->cur ^ 1], nullptr, 0, nullptr);
+      launch_product(M, v->buf[v->cur ^ 1], v->buf[v->cur], nullptr, 0, nullptr);
+    }
+    CU(cudaStreamEndCapture(c->stream, &g));
+    CU(cudaGraphInstantiate(reps == 1 ? &ge2 : &ge32, g, 0));
+    CU(cudaGraphDestroy(g));
+  }
+  for (int w = 0; w < (warmup + 1) / 2; w++) CU(cudaGraphLaunch(ge2, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   cudaEvent_t e0, e1;
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
   const int64_t pairs = (steps + 1) / 2;
   CU(cudaEventRecord(e0, c->stream));
-  for (int64_t k = 0; k < pairs; k++) CU(cudaGraphLaunch(ge, c->stream));
+  for (int64_t k = 0; k < pairs / 16; k++) CU(cudaGraphLaunch(ge32, c->stream));
+  for (int64_t k = 0; k < pairs % 16; k++) CU(cudaGraphLaunch(ge2, c->stream));
   CU(cudaEventRecord(e1, c->stream));
   CU(cudaEventSynchronize(e1));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  cudaGraphExecDestroy(ge);
+  cudaGraphExecDestroy(ge2);
+  cudaGraphExecDestroy(ge32);
   *total_ms = ms;
   *kernel_ms = ms / (2.0 * pairs);
   return SLD_OK;

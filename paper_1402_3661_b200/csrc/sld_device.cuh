@@ -283,11 +283,16 @@ __device__ __forceinline__ void finalize(int64_t (&acc)[L + 1], int64_t S, const
 // resident CTAs per SM the register allocation must allow: 4 x 256 threads
 // (64 registers) for L <= 8 -- the gathers need every warp they can get
 template <int L>
-constexpr int spmv_min_blocks() { return L <= 8 ? 4 : (L <= 16 ? 2 : 1); }
+__host__ __device__ constexpr int spmv_min_blocks() { return L <= 8 ? 4 : (L <= 16 ? 3 : 2); }
+// gathers in flight per thread per batch: 4 for one-sector residues, fewer
+// for wide moduli so the accumulator + gathered slots fit the register budget
+template <int L>
+__host__ __device__ constexpr int spmv_batch() { return L <= 8 ? 4 : (L <= 16 ? 2 : 1); }
 
 template <int L, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const SpmvArgs a, const ModParams mp) {
   constexpr int SW = stride_words(L);
+  constexpr int NB = spmv_batch<L>();
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t slice = slot >> 5;
   const int lane = threadIdx.x & 31;
@@ -319,15 +324,19 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
   for (uint32_t k = 0; k < my_pm; k++) {
     const uint4 w = ld_stream(pp + (size_t)k * 32, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-    uint32_t u[4][SW];
 #pragma unroll
-    for (int e = 0; e < 4; e++) gather_hint<SW>(a.x + (size_t)(ws[e] & 0x7FFFFFFFu) * SW, u[e], gpol);
+    for (int e0 = 0; e0 < 4; e0 += NB) {
+      uint32_t u[NB][SW];
 #pragma unroll
-    for (int e = 0; e < 4; e++) {
-      const int32_t c = 1 - (int32_t)((ws[e] >> 30) & 2u);  // +1 / -1
-      S += c;
+      for (int e = 0; e < NB; e++)
+        gather_hint<SW>(a.x + (size_t)(ws[e0 + e] & 0x7FFFFFFFu) * SW, u[e], gpol);
 #pragma unroll
-      for (int i = 0; i < L; i++) acc[i] += (int64_t)c * (int64_t)(int32_t)u[e][i];
+      for (int e = 0; e < NB; e++) {
+        const int32_t c = 1 - (int32_t)((ws[e0 + e] >> 30) & 2u);  // +1 / -1
+        S += c;
+#pragma unroll
+        for (int i = 0; i < L; i++) acc[i] += (int64_t)c * (int64_t)(int32_t)u[e][i];
+      }
     }
   }
   // small entries: one signed IMAD.WIDE per limb, the 64-bit product split
@@ -340,17 +349,21 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
     const int4 cf = ld_stream(cp + (size_t)k * 32, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
     const int32_t cs[4] = {cf.x, cf.y, cf.z, cf.w};
-    uint32_t u[4][SW];
 #pragma unroll
-    for (int e = 0; e < 4; e++) gather_hint<SW>(a.x + (size_t)ws[e] * SW, u[e], gpol);
+    for (int e0 = 0; e0 < 4; e0 += NB) {
+      uint32_t u[NB][SW];
 #pragma unroll
-    for (int e = 0; e < 4; e++) {
-      S += cs[e];
+      for (int e = 0; e < NB; e++) gather_hint<SW>(a.x + (size_t)ws[e0 + e] * SW, u[e], gpol);
 #pragma unroll
-      for (int i = 0; i < L; i++) {
-        const int64_t p = (int64_t)cs[e] * (int64_t)(int32_t)u[e][i];
-        acc[i] += (int64_t)(uint32_t)p;
-        acc[i + 1] += (int64_t)(int32_t)(p >> 32);
+      for (int e = 0; e < NB; e++) {
+        const int32_t c = cs[e0 + e];
+        S += c;
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+          const int64_t p = (int64_t)c * (int64_t)(int32_t)u[e][i];
+          acc[i] += (int64_t)(uint32_t)p;
+          acc[i + 1] += (int64_t)(int32_t)(p >> 32);
+        }
       }
     }
   }
