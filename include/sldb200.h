@@ -89,10 +89,20 @@ int sld_mat_create(sld_ctx *ctx, int64_t nrows, int64_t ncols,
                    int64_t n_full, const int64_t *full_pos, const uint32_t *full_limbs,
                    int n_dense, const uint32_t *dense_limbs,
                    int64_t max_stripe_cols, sld_mat **out);
+/* Same, laid out for `chains` (1, 2 or 4) interleaved Krylov chains that
+ * share every pass over the matrix: block Wiedemann's independent sequences
+ * (solver.py:220-257) multiplied together, each gather request fetching the
+ * residues of all G chains of a column (G * 32 bytes <= one 128-byte line). */
+int sld_mat_create_chains(sld_ctx *ctx, int chains, int64_t nrows, int64_t ncols,
+                          const int64_t *row_ptr, const int32_t *col_idx,
+                          const uint8_t *tags, const int64_t *small_vals,
+                          int64_t n_full, const int64_t *full_pos, const uint32_t *full_limbs,
+                          int n_dense, const uint32_t *dense_limbs,
+                          int64_t max_stripe_cols, sld_mat **out);
 int sld_mat_destroy(sld_mat *m);
 /* info[0..15]: nrows, total_cols, nnz, n_pm, n_small, n_full(+dense nz),
  * stripes, nslices, device bytes, padded index entries, L, stride words,
- * max row degree, 0, 0, 0 */
+ * max row degree, stripe columns, chains, 0 */
 int sld_mat_info(const sld_mat *m, int64_t *info);
 
 /*
@@ -101,6 +111,10 @@ int sld_mat_info(const sld_mat *m, int64_t *info);
  * 32-bit limbs; planes are repacked on the device.
  */
 int sld_vec_create(sld_ctx *ctx, int64_t n, sld_vec **out);
+/* A vector of `chains` interleaved residue vectors of n each (for matrices
+ * built with sld_mat_create_chains).  Host arrays of such vectors are
+ * chain-major: chains x n x (P or L). */
+int sld_vec_create_chains(sld_ctx *ctx, int64_t n, int chains, sld_vec **out);
 int sld_vec_destroy(sld_vec *v);
 int sld_vec_upload_planes(sld_vec *v, const uint64_t *planes, int64_t n, int P);
 int sld_vec_download_planes(sld_vec *v, uint64_t *planes, int64_t n, int P);
@@ -149,8 +163,9 @@ int sld_spmv_planes(sld_mat *m, const uint64_t *in_planes, uint64_t *out_planes,
  * (solver.py:199-217) with UnitRows projections (solver.py:174-176):
  * for i in [0, steps): terms[i] = X^T v; v = A v.
  *   v: in/out iterate (total_cols == nrows, square matrix).
- *   x_rows[m]: unit projection rows.  terms_limbs: steps*m*L uint32
- *   (host), term i / column t at (i*m + t)*L.
+ *   x_rows[m]: unit projection rows.  terms_limbs: steps*G*m*L uint32
+ *   (host; G = the matrix's chains), step i / chain g / row t at
+ *   ((i*G + g)*m + t)*L.
  * Steps run as CUDA-graph chunks; the call returns after `steps` products.
  */
 int sld_krylov_unit(sld_mat *m, sld_vec *v, const int64_t *x_rows, int mrows,

@@ -14,7 +14,7 @@ from .modring import (
 )
 from .spmatrix import DeviceKernel, SparseMatrix, classify, spmv_planes, spmv_sequential
 from .solver import (
-    B200Multiplier, BlockingParams, BlockSequence, DenseRows, SequentialMultiplier, UnitRows,
+    B200ChainGroup, B200Multiplier, BlockingParams, BlockSequence, DenseRows, SequentialMultiplier, UnitRows,
     draw_blocks, krylov_block, krylov_column, krylov_length, krylov_scalar,
     GeneratorFailure, KernelVector, SolverFailure, mksol_block, mksol_scalar, verify_kernel,
 )

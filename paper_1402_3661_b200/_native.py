@@ -25,8 +25,8 @@ EXPORTS = [
     "sld_version", "sld_last_error", "sld_device_count",
     "sld_ctx_create", "sld_ctx_destroy", "sld_ctx_sync", "sld_ctx_set_stream", "sld_add_mod",
     "sld_vec_read_rows", "sld_lincomb", "sld_vec_nonzero",
-    "sld_mat_create", "sld_mat_destroy", "sld_mat_info",
-    "sld_vec_create", "sld_vec_destroy", "sld_vec_upload_planes", "sld_vec_download_planes",
+    "sld_mat_create", "sld_mat_create_chains", "sld_mat_destroy", "sld_mat_info",
+    "sld_vec_create", "sld_vec_create_chains", "sld_vec_destroy", "sld_vec_upload_planes", "sld_vec_download_planes",
     "sld_vec_upload_limbs", "sld_vec_download_limbs", "sld_vec_device_ptr",
     "sld_spmv", "sld_spmv_planes", "sld_krylov_unit",
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
@@ -76,9 +76,11 @@ def load(build_if_missing=False):
             "sld_lincomb": ([vp, vp, vp, i32, ctypes.c_uint64, ctypes.c_uint64, i64], i32),
             "sld_vec_nonzero": ([vp, vp], i32),
             "sld_mat_create": ([vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, i32, vp, i64, pp], i32),
+            "sld_mat_create_chains": ([vp, i32, i64, i64, vp, vp, vp, vp, i64, vp, vp, i32, vp, i64, pp], i32),
             "sld_mat_destroy": ([vp], i32),
             "sld_mat_info": ([vp, vp], i32),
             "sld_vec_create": ([vp, i64, pp], i32),
+            "sld_vec_create_chains": ([vp, i64, i32, pp], i32),
             "sld_vec_destroy": ([vp], i32),
             "sld_vec_upload_planes": ([vp, u64p, i64, i32], i32),
             "sld_vec_download_planes": ([vp, u64p, i64, i32], i32),

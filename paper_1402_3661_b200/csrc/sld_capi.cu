@@ -132,7 +132,8 @@ struct sld_ctx {
 
 struct sld_vec {
   sld_ctx* ctx = nullptr;
-  int64_t n = 0;
+  int64_t n = 0;      // residues per chain
+  int chains = 1;     // G chains interleaved per record (row*G + chain)
   uint32_t* buf[2] = {nullptr, nullptr};
   int cur = 0;
 };
@@ -151,6 +152,8 @@ struct sld_mat {
   int npass = 1;
   int64_t stripe_cols = 0;
   int64_t nslices = 0;
+  int64_t nslots = 0;
+  int chains = 1;  // G chains per record (built for one G)
   int64_t n_pm = 0, n_small = 0, n_full = 0, pad_entries = 0;
   int64_t max_deg = 0;
   size_t dev_bytes = 0;
@@ -326,24 +329,31 @@ extern "C" int sld_add_mod(sld_ctx* c, const uint64_t* src_ptrs, int k, uint64_t
 
 static int vec_alloc_buf(sld_vec* v, int which) {
   if (v->buf[which]) return SLD_OK;
-  const size_t words = (size_t)(v->n + 1) * v->ctx->SW;
+  const size_t words = (size_t)(v->n + 1) * v->chains * v->ctx->SW;
   CU(cudaMalloc(&v->buf[which], words * 4));
   CU(cudaMemsetAsync(v->buf[which], 0, words * 4, v->ctx->stream));
-  ops(v->ctx->L).zero_slot(v->buf[which] + (size_t)v->n * v->ctx->SW, v->ctx->stream);
+  for (int c = 0; c < v->chains; c++)  // record n: the zero residue of every chain
+    ops(v->ctx->L).zero_slot(v->buf[which] + ((size_t)v->n * v->chains + c) * v->ctx->SW, v->ctx->stream);
   CU(cudaGetLastError());
   return SLD_OK;
 }
 
-extern "C" int sld_vec_create(sld_ctx* ctx, int64_t n, sld_vec** out) {
+extern "C" int sld_vec_create_chains(sld_ctx* ctx, int64_t n, int chains, sld_vec** out) {
   if (!ctx || !out || n < 0) return fail(SLD_E_ARG, "bad vector arguments");
+  if (chains != 1 && chains != 2 && chains != 4) return fail(SLD_E_ARG, "chains must be 1, 2 or 4");
   CU(cudaSetDevice(ctx->dev));
   auto v = std::make_unique<sld_vec>();
   v->ctx = ctx;
   v->n = n;
+  v->chains = chains;
   TRY(vec_alloc_buf(v.get(), 0));
   CU(cudaStreamSynchronize(ctx->stream));
   *out = v.release();
   return SLD_OK;
+}
+
+extern "C" int sld_vec_create(sld_ctx* ctx, int64_t n, sld_vec** out) {
+  return sld_vec_create_chains(ctx, n, 1, out);
 }
 
 extern "C" int sld_vec_destroy(sld_vec* v) {
@@ -401,9 +411,10 @@ static void host_par(int64_t n, F f) {
 static constexpr int64_t XFER_CHUNK = 1 << 19;  // rows per DMA chunk
 
 // rows of planes (P 16-bit digits in uint64 cells) or limbs (L words) -> device slots
-static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs, int64_t n, int P) {
+static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs, int64_t rows, int P) {
   sld_ctx* c = v->ctx;
   const int L = c->L;
+  const int64_t n = rows * v->chains;  // items, chain-major on the host
   const size_t bytes = (size_t)n * L * 4;
   if (!n) return SLD_OK;
   TRY(ensure_stage(c, bytes));
@@ -429,21 +440,22 @@ static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs
     CU(cudaMemcpyAsync(d + (size_t)lo * L, h + (size_t)lo * L, (size_t)(hi - lo) * L * 4,
                        cudaMemcpyHostToDevice, c->stream));
   }
-  ops(L).limbs_to_slots(d, n, v->buf[v->cur], 0x80000000u, c->stream);
+  ops(L).limbs_to_slots(d, n, v->buf[v->cur], 0x80000000u, rows, v->chains, c->stream);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(c->stream));
   return SLD_OK;
 }
 
-static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t n, int P) {
+static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t rows, int P) {
   sld_ctx* c = v->ctx;
   const int L = c->L;
+  const int64_t n = rows * v->chains;
   const size_t bytes = (size_t)n * L * 4;
   if (!n) return SLD_OK;
   TRY(ensure_stage(c, bytes));
   uint32_t* h = (uint32_t*)c->hstage;
   uint32_t* d = (uint32_t*)c->dstage;
-  ops(L).slots_to_limbs(v->buf[v->cur], n, d, 0x80000000u, c->stream);
+  ops(L).slots_to_limbs(v->buf[v->cur], n, d, 0x80000000u, rows, v->chains, c->stream);
   CU(cudaGetLastError());
   std::vector<cudaEvent_t> ev;
   for (int64_t lo = 0; lo < n; lo += XFER_CHUNK) {
@@ -496,7 +508,7 @@ extern "C" int sld_vec_upload_planes(sld_vec* v, const uint64_t* planes, int64_t
 }
 
 extern "C" int sld_vec_download_planes(sld_vec* v, uint64_t* planes, int64_t n, int P) {
-  if (!v || n > v->n || n < 0) return fail(SLD_E_ARG, "plane count mismatch");
+  if (!v || n > v->n || n < 0 || (v->chains > 1 && n != v->n)) return fail(SLD_E_ARG, "plane count mismatch");
   TRY(check_P(v->ctx, P));
   CU(cudaSetDevice(v->ctx->dev));
   return download_rows(v, planes, nullptr, n, P);
@@ -509,7 +521,7 @@ extern "C" int sld_vec_upload_limbs(sld_vec* v, const uint32_t* limbs, int64_t n
 }
 
 extern "C" int sld_vec_download_limbs(sld_vec* v, uint32_t* limbs, int64_t n) {
-  if (!v || n > v->n || n < 0) return fail(SLD_E_ARG, "limb count mismatch");
+  if (!v || n > v->n || n < 0 || (v->chains > 1 && n != v->n)) return fail(SLD_E_ARG, "limb count mismatch");
   CU(cudaSetDevice(v->ctx->dev));
   return download_rows(v, nullptr, limbs, n, 0);
 }
@@ -562,6 +574,7 @@ extern "C" int sld_vec_nonzero(sld_vec* v, int* out) {
 
 extern "C" int sld_vec_read_rows(sld_vec* v, const int64_t* rows, int m, uint32_t* limbs) {
   if (!v || m < 0 || (m && (!rows || !limbs))) return fail(SLD_E_ARG, "bad read_rows arguments");
+  if (v->chains != 1) return fail(SLD_E_ARG, "read_rows needs a single-chain vector");
   for (int t = 0; t < m; t++)
     if (rows[t] < 0 || rows[t] >= v->n) return fail(SLD_E_ARG, "row out of range");
   if (!m) return SLD_OK;
@@ -630,6 +643,15 @@ static void mat_free(sld_mat* m) {
   delete m;
 }
 
+extern "C" int sld_mat_create(sld_ctx* ctx, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                              const int32_t* col_idx, const uint8_t* tags, const int64_t* small_vals,
+                              int64_t n_full, const int64_t* full_pos, const uint32_t* full_limbs,
+                              int n_dense, const uint32_t* dense_limbs, int64_t max_stripe_cols,
+                              sld_mat** out) {
+  return sld_mat_create_chains(ctx, 1, nrows, ncols, row_ptr, col_idx, tags, small_vals, n_full,
+                               full_pos, full_limbs, n_dense, dense_limbs, max_stripe_cols, out);
+}
+
 extern "C" int sld_mat_destroy(sld_mat* m) {
   if (!m) return SLD_OK;
   cudaSetDevice(m->ctx->dev);
@@ -668,7 +690,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     // measured (tools/sweep.py): one pass while the gathered vector fits in
     // ~80% of L2 (cfg2 21 MB, cfg5 96 MB); beyond that, stripes of <= 1/2 L2
     // (cfg3: 2 x 58 MB) so each pass's working set stays L2-resident
-    const double vec_bytes = (double)(M->total_cols + 1) * SW * 4.0;
+    const double vec_bytes = (double)(M->total_cols + 1) * SW * 4.0 * M->chains;
     if (vec_bytes <= 0.80 * (double)c->l2_bytes) {
       stripe = ncols;
     } else {
@@ -740,9 +762,11 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     if (tot_pm[x] != tot_pm[y]) return tot_pm[x] > tot_pm[y];
     return tot_s[x] > tot_s[y];
   });
-  const int64_t nslices = (nrows + 31) / 32;
+  const int RH = 32 / M->chains;  // rows per slice (one warp: RH rows x G chains)
+  const int64_t nslices = (nrows + RH - 1) / RH;
   M->nslices = nslices;
-  const int64_t nslots = nslices * 32;
+  const int64_t nslots = nslices * RH;
+  M->nslots = nslots;
   std::vector<int32_t> slot_row(nslots, -1);
   for (int64_t s = 0; s < nrows; s++) slot_row[s] = order[s];
   // ---- slice tables
@@ -751,8 +775,8 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   for (int p = 0; p < npass; p++) {
     for (int64_t s = 0; s < nslices; s++) {
       uint32_t kpm = 0, ks = 0;
-      for (int l = 0; l < 32; l++) {
-        const int32_t r = slot_row[s * 32 + l];
+      for (int l = 0; l < RH; l++) {
+        const int32_t r = slot_row[s * RH + l];
         if (r < 0) continue;
         kpm = std::max(kpm, (rc.pm[(size_t)p * nrows + r] + 3) / 4);
         ks = std::max(ks, (rc.sm[(size_t)p * nrows + r] + 3) / 4);
@@ -762,8 +786,8 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
       si.pm_k4 = kpm;
       si.s_off = (uint32_t)s_units;
       si.s_k4 = ks;
-      pm_units += (uint64_t)kpm * 32;
-      s_units += (uint64_t)ks * 32;
+      pm_units += (uint64_t)kpm * RH;
+      s_units += (uint64_t)ks * RH;
       if (pm_units >= (1ull << 32) || s_units >= (1ull << 32))
         return fail(SLD_E_BOUND, "matrix too large for 32-bit slice offsets");
     }
@@ -798,8 +822,8 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     for (int64_t slot = lo; slot < hi; slot++) {
       const int32_t r = slot_row[slot];
       if (r < 0) continue;
-      const int64_t slice = slot >> 5;
-      const int lane = (int)(slot & 31);
+      const int64_t slice = slot / RH;
+      const int lane = (int)(slot % RH);
       std::fill(kp.begin(), kp.end(), 0u);
       std::fill(ks.begin(), ks.end(), 0u);
       uint32_t fk = full_ptr[slot];
@@ -810,7 +834,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
         const SliceInfo& si = slices[(size_t)pass * nslices + slice];
         if (t <= 1) {
           const uint32_t k = kp[pass]++;
-          const uint64_t pos = ((uint64_t)si.pm_off + (uint64_t)(k >> 2) * 32 + lane) * 4 + (k & 3);
+          const uint64_t pos = ((uint64_t)si.pm_off + (uint64_t)(k >> 2) * RH + lane) * 4 + (k & 3);
           pm_idx[pos] = col | (t == 1 ? 0x80000000u : 0u);
           continue;
         }
@@ -818,7 +842,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
           const int64_t v = small_vals[p];
           if (v > -0x80000000ll && v < 0x80000000ll) {
             const uint32_t k = ks[pass]++;
-            const uint64_t pos = ((uint64_t)si.s_off + (uint64_t)(k >> 2) * 32 + lane) * 4 + (k & 3);
+            const uint64_t pos = ((uint64_t)si.s_off + (uint64_t)(k >> 2) * RH + lane) * 4 + (k & 3);
             s_idx[pos] = col;
             s_coef[pos] = (int32_t)v;
             continue;
@@ -905,8 +929,8 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     ops(L).to_mont(M->dense_val, (int64_t)M->n_dense * nslots, c->mp, c->stream);
   }
   if (npass > 1) {
-    CU(cudaMalloc(&M->part, (size_t)nslots * SW * 4));
-    acct += (size_t)nslots * SW * 4;
+    CU(cudaMalloc(&M->part, (size_t)nslots * M->chains * SW * 4));
+    acct += (size_t)nslots * M->chains * SW * 4;
   }
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(c->stream));
@@ -914,11 +938,16 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   return SLD_OK;
 }
 
-extern "C" int sld_mat_create(sld_ctx* ctx, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
-                              const int32_t* col_idx, const uint8_t* tags, const int64_t* small_vals,
-                              int64_t n_full, const int64_t* full_pos, const uint32_t* full_limbs,
-                              int n_dense, const uint32_t* dense_limbs, int64_t max_stripe_cols,
-                              sld_mat** out) {
+extern "C" int sld_mat_create_chains(sld_ctx* ctx, int chains, int64_t nrows, int64_t ncols,
+                                     const int64_t* row_ptr, const int32_t* col_idx, const uint8_t* tags,
+                                     const int64_t* small_vals, int64_t n_full, const int64_t* full_pos,
+                                     const uint32_t* full_limbs, int n_dense, const uint32_t* dense_limbs,
+                                     int64_t max_stripe_cols, sld_mat** out) {
+  if (!ctx) return fail(SLD_E_ARG, "null context");
+  if (chains != 1 && chains != 2 && chains != 4)
+    return fail(SLD_E_ARG, "chains must be 1, 2 or 4");
+  if (chains > max_chains(ctx->L))
+    return fail(SLD_E_ARG, "%d chains per record exceed one 128-byte line at %d limbs", chains, ctx->L);
   if (!ctx || !out || !row_ptr || nrows < 0 || ncols < 0 || n_dense < 0 || n_full < 0)
     return fail(SLD_E_ARG, "bad matrix arguments");
   if (nrows >= 0x7FFFFFFF || ncols + n_dense >= 0x7FFFFFFF)
@@ -930,6 +959,7 @@ extern "C" int sld_mat_create(sld_ctx* ctx, int64_t nrows, int64_t ncols, const 
   CU(cudaSetDevice(ctx->dev));
   sld_mat* M = new sld_mat();
   M->ctx = ctx;
+  M->chains = chains;
   M->nrows = nrows;
   M->ncols = ncols;
   M->n_dense = n_dense;
@@ -952,7 +982,7 @@ extern "C" int sld_mat_info(const sld_mat* m, int64_t* info) {
   if (!m || !info) return fail(SLD_E_ARG, "null argument");
   int64_t v[16] = {m->nrows, m->total_cols, m->nnz, m->n_pm, m->n_small, m->n_full,
                    m->npass, m->nslices, (int64_t)m->dev_bytes, m->pad_entries,
-                   m->ctx->L, m->ctx->SW, m->max_deg, m->stripe_cols, 0, 0};
+                   m->ctx->L, m->ctx->SW, m->max_deg, m->stripe_cols, m->chains, 0};
   memcpy(info, v, sizeof(v));
   return SLD_OK;
 }
@@ -983,6 +1013,7 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
   a.proj_m = proj_m;
   a.terms_out = terms_out;
   a.nslices = M->nslices;
+  a.nslots = M->nslots;
   a.has_full = (M->full_ptr && M->n_full) ? 1 : 0;
   a.policy = M->policy;
   const LOps& o = ops(c->L);
@@ -992,13 +1023,13 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
       a.nslices = 0;
       a.slices = M->slices;
       a.lane_k4 = M->lane_k4;
-      o.pass(1, 1, 1, c->stream, a, c->mp);
+      o.pass(M->chains, 1, 1, 1, c->stream, a, c->mp);
     }
     return;
   }
   for (int p = 0; p < M->npass; p++) {
     a.slices = M->slices + (size_t)p * M->nslices;
-    a.lane_k4 = M->lane_k4 + (size_t)p * M->nslices * 32;
+    a.lane_k4 = M->lane_k4 + (size_t)p * M->nslots;
     if (M->apw && c->apw_max) {
       // persisting L2 window over the stripe this pass gathers from
       const int64_t lo = (int64_t)p * M->stripe_cols;
@@ -1012,7 +1043,7 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
       v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
     }
-    o.pass(p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
+    o.pass(M->chains, p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
   }
   if (M->apw && c->apw_max) {
     cudaStreamAttrValue v;
@@ -1029,6 +1060,8 @@ extern "C" int sld_spmv(sld_mat* M, sld_vec* in, sld_vec* out) {
   if (out->n < M->nrows) return fail(SLD_E_ARG, "output vector too short");
   if (in == out) return fail(SLD_E_ARG, "in and out must differ");
   if (in->ctx != M->ctx || out->ctx != M->ctx) return fail(SLD_E_ARG, "context mismatch");
+  if (in->chains != M->chains || out->chains != M->chains)
+    return fail(SLD_E_ARG, "vector chains (%d, %d) != matrix chains %d", in->chains, out->chains, M->chains);
   CU(cudaSetDevice(M->ctx->dev));
   launch_product(M, in->buf[in->cur], out->buf[out->cur], nullptr, 0, nullptr);
   CU(cudaGetLastError());
@@ -1041,8 +1074,8 @@ extern "C" int sld_spmv_planes(sld_mat* M, const uint64_t* in_planes, uint64_t* 
   sld_ctx* c = M->ctx;
   TRY(check_P(c, P));
   CU(cudaSetDevice(c->dev));
-  if (!M->tmp_in) TRY(sld_vec_create(c, M->total_cols, &M->tmp_in));
-  if (!M->tmp_out) TRY(sld_vec_create(c, M->nrows, &M->tmp_out));
+  if (!M->tmp_in) TRY(sld_vec_create_chains(c, M->total_cols, M->chains, &M->tmp_in));
+  if (!M->tmp_out) TRY(sld_vec_create_chains(c, M->nrows, M->chains, &M->tmp_out));
   TRY(upload_rows(M->tmp_in, in_planes, nullptr, M->total_cols, P));
   launch_product(M, M->tmp_in->buf[0], M->tmp_out->buf[0], nullptr, 0, nullptr);
   CU(cudaGetLastError());
@@ -1054,7 +1087,7 @@ extern "C" int sld_spmv_planes(sld_mat* M, const uint64_t* in_planes, uint64_t* 
 
 static int ensure_proj(sld_mat* M, const int64_t* x_rows, int m, int64_t chunk) {
   sld_ctx* c = M->ctx;
-  if (m > 256) return fail(SLD_E_ARG, "at most 256 unit projection rows");
+  if (m * M->chains > 256) return fail(SLD_E_ARG, "at most 256 projected residues per product");
   for (int t = 0; t < m; t++)
     if (x_rows[t] < 0 || x_rows[t] >= M->total_cols) return fail(SLD_E_ARG, "projection row out of range");
   if (M->proj_cap < m) {
@@ -1064,7 +1097,7 @@ static int ensure_proj(sld_mat* M, const int64_t* x_rows, int m, int64_t chunk) 
     M->proj_cap = m;
   }
   if (m) CU(cudaMemcpyAsync(M->proj_rows, x_rows, m * 8, cudaMemcpyHostToDevice, c->stream));
-  const size_t need = (size_t)std::max<int64_t>(chunk, 1) * std::max(m, 1) * c->SW;
+  const size_t need = (size_t)std::max<int64_t>(chunk, 1) * std::max(m, 1) * M->chains * c->SW;
   if (M->terms_cap < need) {
     if (M->terms_dev) cudaFree(M->terms_dev);
     M->terms_dev = nullptr;
@@ -1074,11 +1107,13 @@ static int ensure_proj(sld_mat* M, const int64_t* x_rows, int m, int64_t chunk) 
   return SLD_OK;
 }
 
-// copy `steps` terms from device (SW stride, at `src`) into host limbs
+// copy `steps` terms from device ([step][t][chain], SW stride, at `src`) into
+// host limbs laid out [step][chain][t][L]
 static int drain_terms(sld_mat* M, const uint32_t* src, int m, int64_t steps, uint32_t* host,
                        std::vector<uint32_t>& tmp) {
   sld_ctx* c = M->ctx;
-  const size_t words = (size_t)steps * m * c->SW;
+  const int G = M->chains;
+  const size_t words = (size_t)steps * m * G * c->SW;
   if (!words) {
     CU(cudaStreamSynchronize(c->stream));
     return SLD_OK;
@@ -1087,8 +1122,13 @@ static int drain_terms(sld_mat* M, const uint32_t* src, int m, int64_t steps, ui
   CU(cudaMemcpyAsync(tmp.data(), src, words * 4, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   const int L = c->L, SW = c->SW;
-  for (int64_t k = 0; k < steps * m; k++)
-    for (int i = 0; i < L; i++) host[k * L + i] = tmp[k * SW + i];
+  for (int64_t k = 0; k < steps; k++)
+    for (int t = 0; t < m; t++)
+      for (int g = 0; g < G; g++) {
+        const uint32_t* a = &tmp[(((size_t)k * m + t) * G + g) * SW];
+        uint32_t* b = host + (((size_t)k * G + g) * m + t) * L;
+        for (int i = 0; i < L; i++) b[i] = a[i];
+      }
   return SLD_OK;
 }
 
@@ -1101,13 +1141,14 @@ extern "C" int sld_krylov_unit(sld_mat* M, sld_vec* v, const int64_t* x_rows, in
   if (M->nrows != M->total_cols) return fail(SLD_E_ARG, "Krylov needs a square matrix");
   if (v->n != M->total_cols) return fail(SLD_E_ARG, "iterate length mismatch");
   if (v->ctx != M->ctx) return fail(SLD_E_ARG, "context mismatch");
+  if (v->chains != M->chains) return fail(SLD_E_ARG, "vector chains != matrix chains");
   if (m && (!x_rows || !terms)) return fail(SLD_E_ARG, "null projection arrays");
   sld_ctx* c = M->ctx;
   CU(cudaSetDevice(c->dev));
   TRY(vec_alloc_buf(v, v->cur ^ 1));
   // terms_dev: [0, GRAPH_STEPS) graph scratch, then the chunk accumulation area
   TRY(ensure_proj(M, x_rows, m, GRAPH_STEPS + KRYLOV_CHUNK));
-  const size_t tstride = (size_t)m * c->SW;  // words per step
+  const size_t tstride = (size_t)m * M->chains * c->SW;  // words per step
   uint32_t* scratch = M->terms_dev;
   uint32_t* area = M->terms_dev + (size_t)GRAPH_STEPS * tstride;
   std::vector<uint32_t> tmp;
@@ -1147,7 +1188,7 @@ extern "C" int sld_krylov_unit(sld_mat* M, sld_vec* v, const int64_t* x_rows, in
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { rc = fail(SLD_E_CUDA, "launch: %s", cudaGetErrorString(e)); break; }
-    rc = drain_terms(M, area, m, chunk, m ? terms + (size_t)done * m * c->L : nullptr, tmp);
+    rc = drain_terms(M, area, m, chunk, m ? terms + (size_t)done * m * M->chains * c->L : nullptr, tmp);
     done += chunk;
   }
   for (auto& x : exec)
@@ -1171,7 +1212,7 @@ extern "C" int sld_xblock_create(sld_ctx* ctx, const uint32_t* x_limbs, int m, i
     uint32_t* d = nullptr;
     CU(cudaMalloc(&d, cnt * ctx->L * 4));
     CU(cudaMemcpyAsync(d, x_limbs, cnt * ctx->L * 4, cudaMemcpyHostToDevice, ctx->stream));
-    ops(ctx->L).limbs_to_slots(d, (int64_t)cnt, xb->x, 0u, ctx->stream);
+    ops(ctx->L).limbs_to_slots(d, (int64_t)cnt, xb->x, 0u, (int64_t)cnt, 1, ctx->stream);
     ops(ctx->L).to_mont(xb->x, (int64_t)cnt, ctx->mp, ctx->stream);
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     cudaFree(d);
@@ -1193,6 +1234,7 @@ extern "C" int sld_krylov_dense(sld_mat* M, sld_vec* v, sld_xblock* X, int64_t s
   if (!M || !v || !X || steps < 0) return fail(SLD_E_ARG, "bad Krylov arguments");
   if (M->nrows != M->total_cols) return fail(SLD_E_ARG, "Krylov needs a square matrix");
   if (v->n != M->total_cols || X->n != M->total_cols) return fail(SLD_E_ARG, "length mismatch");
+  if (M->chains != 1 || v->chains != 1) return fail(SLD_E_ARG, "dense projection runs one chain per matrix");
   sld_ctx* c = M->ctx;
   CU(cudaSetDevice(c->dev));
   TRY(vec_alloc_buf(v, v->cur ^ 1));
@@ -1236,6 +1278,7 @@ extern "C" int sld_bench_spmv(sld_mat* M, sld_vec* v, int64_t steps, int warmup,
                               double* kernel_ms) {
   if (!M || !v || steps < 1) return fail(SLD_E_ARG, "bad bench arguments");
   if (M->nrows != M->total_cols || v->n != M->total_cols) return fail(SLD_E_ARG, "square matrix needed");
+  if (v->chains != M->chains) return fail(SLD_E_ARG, "vector chains != matrix chains");
   sld_ctx* c = M->ctx;
   CU(cudaSetDevice(c->dev));
   TRY(vec_alloc_buf(v, v->cur ^ 1));

@@ -59,6 +59,7 @@ struct SpmvArgs {
   int proj_m;
   uint32_t* terms_out;      // proj_m slots of SW words, canonical (unbiased)
   int64_t nslices;
+  int64_t nslots;  // nslices * rows per slice (dense-value row stride)
   int has_full;
   int policy;  // bit0 gather L2 evict_last, bit1 output store evict_first,
                // bit2 partial store evict_first, bit3 gathers L1::no_allocate
@@ -289,18 +290,28 @@ __host__ __device__ constexpr int spmv_min_blocks() { return L <= 8 ? 4 : (L <= 
 template <int L>
 __host__ __device__ constexpr int spmv_batch() { return L <= 8 ? 4 : (L <= 16 ? 2 : 1); }
 
-template <int L, bool FIRST, bool LAST>
+// G chains share one matrix pass (block Wiedemann's independent sequences):
+// a column's G residues are one contiguous record of G*SW words, and the G
+// lanes of a row gather the G sectors of the same record in one instruction,
+// which the L1 coalesces into ONE request.  Random gathers are request-bound
+// (~1 sector-request per SM per clock, profiles/microbench2_r01.txt), so a
+// 2-sector record moves ~1.7x the useful bytes per second of a 1-sector one.
+template <int L, int G, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const SpmvArgs a, const ModParams mp) {
   constexpr int SW = stride_words(L);
   constexpr int NB = spmv_batch<L>();
-  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t slice = slot >> 5;
+  constexpr int R = 32 / G;  // rows per warp = slice height
   const int lane = threadIdx.x & 31;
+  const int chain = lane & (G - 1);
+  const int rw = lane / G;
+  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t slot = slice * R + rw;
 
-  if (FIRST && blockIdx.x == 0 && threadIdx.x < a.proj_m) {
+  if (FIRST && blockIdx.x == 0 && threadIdx.x < a.proj_m * G) {
     // a_i = X^T v_i of the iterate this product consumes (solver.py:210)
-    const uint32_t* src = a.x + (size_t)a.proj_rows[threadIdx.x] * SW;
-    uint32_t* dst = a.terms_out + (size_t)threadIdx.x * SW;
+    const int t = threadIdx.x / G, c = threadIdx.x % G;
+    const uint32_t* src = a.x + ((size_t)a.proj_rows[t] * G + c) * SW;
+    uint32_t* dst = a.terms_out + ((size_t)t * G + c) * SW;
 #pragma unroll
     for (int i = 0; i < SW; i++) dst[i] = i < L ? (src[i] ^ 0x80000000u) : 0u;
   }
@@ -309,27 +320,28 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
   const uint64_t pol = policy_evict_first();
   const uint64_t gpol = (a.policy & 1) ? policy_evict_last() : createpolicy_normal();
   const SliceInfo si = a.slices[slice];
-  // per-lane group counts: lanes stop at their own row length, so padded
+  // per-row group counts: lanes stop at their own row length, so padded
   // SELL positions are never loaded (no index or gather traffic)
   const uint32_t kk = a.lane_k4[slot];
   const uint32_t my_pm = kk & 0xFFFFu, my_s = kk >> 16;
+  const uint32_t* xc = a.x + (size_t)chain * SW;  // this lane's chain in every record
   int64_t acc[L + 1];
 #pragma unroll
   for (int i = 0; i <= L; i++) acc[i] = 0;
   int64_t S = 0;  // sum of coefficients (bias correction)
 
   // +-1 entries
-  const uint4* pp = a.pm_idx + si.pm_off + lane;
+  const uint4* pp = a.pm_idx + si.pm_off + rw;
 #pragma unroll 1
   for (uint32_t k = 0; k < my_pm; k++) {
-    const uint4 w = ld_stream(pp + (size_t)k * 32, pol);
+    const uint4 w = ld_stream(pp + (size_t)k * R, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
     for (int e0 = 0; e0 < 4; e0 += NB) {
       uint32_t u[NB][SW];
 #pragma unroll
       for (int e = 0; e < NB; e++)
-        gather_hint<SW>(a.x + (size_t)(ws[e0 + e] & 0x7FFFFFFFu) * SW, u[e], gpol);
+        gather_hint<SW>(xc + (size_t)(ws[e0 + e] & 0x7FFFFFFFu) * (G * SW), u[e], gpol);
 #pragma unroll
       for (int e = 0; e < NB; e++) {
         const int32_t c = 1 - (int32_t)((ws[e0 + e] >> 30) & 2u);  // +1 / -1
@@ -341,19 +353,19 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
   }
   // small entries: one signed IMAD.WIDE per limb, the 64-bit product split
   // into its low word (limb i) and signed high word (limb i+1)
-  const uint4* sp = a.s_idx + si.s_off + lane;
-  const int4* cp = a.s_coef + si.s_off + lane;
+  const uint4* sp = a.s_idx + si.s_off + rw;
+  const int4* cp = a.s_coef + si.s_off + rw;
 #pragma unroll 1
   for (uint32_t k = 0; k < my_s; k++) {
-    const uint4 w = ld_stream(sp + (size_t)k * 32, pol);
-    const int4 cf = ld_stream(cp + (size_t)k * 32, pol);
+    const uint4 w = ld_stream(sp + (size_t)k * R, pol);
+    const int4 cf = ld_stream(cp + (size_t)k * R, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
     const int32_t cs[4] = {cf.x, cf.y, cf.z, cf.w};
 #pragma unroll
     for (int e0 = 0; e0 < 4; e0 += NB) {
       uint32_t u[NB][SW];
 #pragma unroll
-      for (int e = 0; e < NB; e++) gather_hint<SW>(a.x + (size_t)ws[e0 + e] * SW, u[e], gpol);
+      for (int e = 0; e < NB; e++) gather_hint<SW>(xc + (size_t)ws[e0 + e] * (G * SW), u[e], gpol);
 #pragma unroll
       for (int e = 0; e < NB; e++) {
         const int32_t c = cs[e0 + e];
@@ -369,7 +381,7 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
   }
   if (!FIRST) {
     uint32_t pin[SW];
-    load_slot<SW>(a.part_in + (size_t)slot * SW, pin, pol);
+    load_slot<SW>(a.part_in + ((size_t)slot * G + chain) * SW, pin, pol);
 #pragma unroll
     for (int i = 0; i < L; i++) acc[i] += pin[i];
   }
@@ -379,7 +391,7 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
 #pragma unroll 1
     for (uint32_t p = a.full_ptr[slot]; p < a.full_ptr[slot + 1]; p++) {
       uint32_t u[SW], f[L], r[L];
-      gather<SW>(a.x + (size_t)a.full_col[p] * SW, u);
+      gather<SW>(xc + (size_t)a.full_col[p] * (G * SW), u);
 #pragma unroll
       for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; f[i] = a.full_val[(size_t)p * SW + i]; }
       montmul<L>(f, u, mp, r);
@@ -390,11 +402,11 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
 #pragma unroll 1
       for (int g = 0; g < a.n_dense; g++) {
         uint32_t u[SW], f[L], r[L];
-        gather<SW>(a.x + (size_t)(a.dense_col0 + g) * SW, u);
+        gather<SW>(xc + (size_t)(a.dense_col0 + g) * (G * SW), u);
 #pragma unroll
         for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; }
-        // dense values: [g][row], rows padded to nslices*32
-        const uint32_t* dv = a.dense_val + ((size_t)g * (size_t)a.nslices * 32 + (size_t)row) * SW;
+        // dense values: [g][row], rows padded to nslots
+        const uint32_t* dv = a.dense_val + ((size_t)g * (size_t)a.nslots + (size_t)row) * SW;
 #pragma unroll
         for (int i = 0; i < L; i++) f[i] = dv[i];
         montmul<L>(f, u, mp, r);
@@ -403,78 +415,51 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
       }
     }
   }
-  uint32_t R[L];
-  finalize<L>(acc, S, mp, R);
+  uint32_t Rr[L];
+  finalize<L>(acc, S, mp, Rr);
   uint32_t o[SW];
   if (LAST) {
     if (row < 0) return;
 #pragma unroll
-    for (int i = 0; i < SW; i++) o[i] = i < L ? (R[i] ^ 0x80000000u) : 0u;
-    if (a.policy & 2) store_slot_hint<SW>(a.y + (size_t)row * SW, o, pol);
-    else store_slot<SW>(a.y + (size_t)row * SW, o);
+    for (int i = 0; i < SW; i++) o[i] = i < L ? (Rr[i] ^ 0x80000000u) : 0u;
+    uint32_t* dst = a.y + ((size_t)row * G + chain) * SW;
+    if (a.policy & 2) store_slot_hint<SW>(dst, o, pol);
+    else store_slot<SW>(dst, o);
   } else {
 #pragma unroll
-    for (int i = 0; i < SW; i++) o[i] = i < L ? R[i] : 0u;
-    if (a.policy & 4) store_slot_hint<SW>(a.part_out + (size_t)slot * SW, o, pol);
-    else store_slot<SW>(a.part_out + (size_t)slot * SW, o);
+    for (int i = 0; i < SW; i++) o[i] = i < L ? Rr[i] : 0u;
+    uint32_t* dst = a.part_out + ((size_t)slot * G + chain) * SW;
+    if (a.policy & 4) store_slot_hint<SW>(dst, o, pol);
+    else store_slot<SW>(dst, o);
   }
 }
 
 // ------------------------------------------------------ conversion kernels
 
-// digit planes (n x P uint64, one 16-bit digit per cell) -> biased slots
-template <int L>
-__global__ void planes_to_slots(const uint64_t* __restrict__ planes, int P, int64_t n,
-                                uint32_t* __restrict__ out) {
-  constexpr int SW = stride_words(L);
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t* src = planes + (size_t)i * P;
-  uint32_t o[SW];
-#pragma unroll
-  for (int j = 0; j < SW; j++) {
-    uint32_t lo = 2 * j < P ? (uint32_t)(src[2 * j] & 0xFFFF) : 0u;
-    uint32_t hi = 2 * j + 1 < P ? (uint32_t)(src[2 * j + 1] & 0xFFFF) : 0u;
-    o[j] = j < L ? ((lo | (hi << 16)) ^ 0x80000000u) : 0u;
-  }
-  store_slot<SW>(out + (size_t)i * SW, o);
-}
-
-template <int L>
-__global__ void slots_to_planes(const uint32_t* __restrict__ in, int64_t n, int P,
-                                uint64_t* __restrict__ planes) {
-  constexpr int SW = stride_words(L);
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t* src = in + (size_t)i * SW;
-  uint64_t* dst = planes + (size_t)i * P;
-  for (int d = 0; d < P; d++) {
-    const int j = d >> 1;
-    uint32_t w = j < L ? (src[j] ^ 0x80000000u) : 0u;
-    dst[d] = (d & 1) ? (w >> 16) : (w & 0xFFFF);
-  }
-}
-
+// item i of a chain-major host array (chain i / rows, row i % rows) lives in
+// slot record row * G + chain on the device
 template <int L>
 __global__ void limbs_to_slots(const uint32_t* __restrict__ limbs, int64_t n, uint32_t* __restrict__ out,
-                               uint32_t bias) {
+                               uint32_t bias, int64_t rows, int G) {
   constexpr int SW = stride_words(L);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int64_t slot = (i % rows) * G + i / rows;
   uint32_t o[SW];
 #pragma unroll
   for (int j = 0; j < SW; j++) o[j] = j < L ? (limbs[(size_t)i * L + j] ^ bias) : 0u;
-  store_slot<SW>(out + (size_t)i * SW, o);
+  store_slot<SW>(out + (size_t)slot * SW, o);
 }
 
 template <int L>
 __global__ void slots_to_limbs(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ limbs,
-                               uint32_t bias) {
+                               uint32_t bias, int64_t rows, int G) {
   constexpr int SW = stride_words(L);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int64_t slot = (i % rows) * G + i / rows;
 #pragma unroll
-  for (int j = 0; j < L; j++) limbs[(size_t)i * L + j] = in[(size_t)i * SW + j] ^ bias;
+  for (int j = 0; j < L; j++) limbs[(size_t)i * L + j] = in[(size_t)slot * SW + j] ^ bias;
 }
 
 // in-place Montgomery conversion f -> f R mod ell = montmul(f, R^2)

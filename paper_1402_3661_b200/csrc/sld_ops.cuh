@@ -9,13 +9,16 @@
 
 namespace sld {
 
+// chains per record the SpMV supports for L limbs: a record must fit one
+// 128-byte line (G * SW * 4 <= 128), so G = 2 up to 16 limbs, 4 up to 8
+__host__ __device__ constexpr int max_chains(int L) { return L <= 8 ? 4 : (L <= 16 ? 2 : 1); }
+
 struct LOps {
-  void (*pass)(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
+  // returns false if G is not supported for this L
+  bool (*pass)(int G, int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
                const ModParams& mp);
-  void (*planes_to_slots)(const uint64_t*, int, int64_t, uint32_t*, cudaStream_t);
-  void (*slots_to_planes)(const uint32_t*, int64_t, int, uint64_t*, cudaStream_t);
-  void (*limbs_to_slots)(const uint32_t*, int64_t, uint32_t*, uint32_t, cudaStream_t);
-  void (*slots_to_limbs)(const uint32_t*, int64_t, uint32_t*, uint32_t, cudaStream_t);
+  void (*limbs_to_slots)(const uint32_t*, int64_t, uint32_t*, uint32_t, int64_t, int, cudaStream_t);
+  void (*slots_to_limbs)(const uint32_t*, int64_t, uint32_t*, uint32_t, int64_t, int, cudaStream_t);
   void (*to_mont)(uint32_t*, int64_t, const ModParams&, cudaStream_t);
   void (*zero_slot)(uint32_t*, cudaStream_t);
   void (*dense_proj)(const DenseProjArgs&, const ModParams&, cudaStream_t);
@@ -27,28 +30,45 @@ struct LOps {
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+template <int L, int G>
+void launch_pass(int first, int last, unsigned grid, cudaStream_t s, const SpmvArgs& a,
+                 const ModParams& mp) {
+  if (first && last) spmv_pass<L, G, true, true><<<grid, 256, 0, s>>>(a, mp);
+  else if (first) spmv_pass<L, G, true, false><<<grid, 256, 0, s>>>(a, mp);
+  else if (last) spmv_pass<L, G, false, true><<<grid, 256, 0, s>>>(a, mp);
+  else spmv_pass<L, G, false, false><<<grid, 256, 0, s>>>(a, mp);
+}
+
 template <int L>
 struct Ops {
-  static void pass(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
+  static bool pass(int G, int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
                    const ModParams& mp) {
-    const unsigned grid = blocks_for(nslices * 32, 256);
-    if (grid == 0) return;
-    if (first && last) spmv_pass<L, true, true><<<grid, 256, 0, s>>>(a, mp);
-    else if (first) spmv_pass<L, true, false><<<grid, 256, 0, s>>>(a, mp);
-    else if (last) spmv_pass<L, false, true><<<grid, 256, 0, s>>>(a, mp);
-    else spmv_pass<L, false, false><<<grid, 256, 0, s>>>(a, mp);
+    const unsigned grid = blocks_for(nslices * 32, 256);  // one warp per slice
+    if (G == 1) {
+      if (grid) launch_pass<L, 1>(first, last, grid, s, a, mp);
+      return true;
+    }
+    if constexpr (max_chains(L) >= 2) {
+      if (G == 2) {
+        if (grid) launch_pass<L, 2>(first, last, grid, s, a, mp);
+        return true;
+      }
+    }
+    if constexpr (max_chains(L) >= 4) {
+      if (G == 4) {
+        if (grid) launch_pass<L, 4>(first, last, grid, s, a, mp);
+        return true;
+      }
+    }
+    return false;
   }
-  static void p2s(const uint64_t* p, int P, int64_t n, uint32_t* o, cudaStream_t s) {
-    if (n) planes_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(p, P, n, o);
+  static void l2s(const uint32_t* l, int64_t n, uint32_t* o, uint32_t b, int64_t rows, int G,
+                  cudaStream_t s) {
+    if (n) limbs_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(l, n, o, b, rows, G);
   }
-  static void s2p(const uint32_t* i, int64_t n, int P, uint64_t* p, cudaStream_t s) {
-    if (n) slots_to_planes<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, P, p);
-  }
-  static void l2s(const uint32_t* l, int64_t n, uint32_t* o, uint32_t b, cudaStream_t s) {
-    if (n) limbs_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(l, n, o, b);
-  }
-  static void s2l(const uint32_t* i, int64_t n, uint32_t* l, uint32_t b, cudaStream_t s) {
-    if (n) slots_to_limbs<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, l, b);
+  static void s2l(const uint32_t* i, int64_t n, uint32_t* l, uint32_t b, int64_t rows, int G,
+                  cudaStream_t s) {
+    if (n) slots_to_limbs<L><<<blocks_for(n, 256), 256, 0, s>>>(i, n, l, b, rows, G);
   }
   static void mont(uint32_t* x, int64_t n, const ModParams& mp, cudaStream_t s) {
     if (n) to_montgomery<L><<<blocks_for(n, 128), 128, 0, s>>>(x, n, mp);
@@ -69,7 +89,7 @@ struct Ops {
   static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
     if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);
   }
-  static LOps make() { return LOps{pass, p2s, s2p, l2s, s2l, mont, zero, dproj, addm, rrows, lcomb, nz}; }
+  static LOps make() { return LOps{pass, l2s, s2l, mont, zero, dproj, addm, rrows, lcomb, nz}; }
 };
 
 template <int L, int LMIN>

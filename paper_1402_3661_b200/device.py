@@ -85,13 +85,15 @@ class Field:
 
 
 class DeviceVector:
-    """A device vector of n residues (biased 32-bit limbs, sector padded)."""
+    """A device vector of n residues (biased 32-bit limbs, sector padded);
+    with chains = G, G interleaved vectors (host arrays chain-major)."""
 
-    def __init__(self, field: Field, n: int):
+    def __init__(self, field: Field, n: int, chains: int = 1):
         self.field = field
         self.n = int(n)
+        self.chains = int(chains)
         h = ctypes.c_void_p()
-        N.check(N.load().sld_vec_create(field.handle, self.n, ctypes.byref(h)))
+        N.check(N.load().sld_vec_create_chains(field.handle, self.n, self.chains, ctypes.byref(h)))
         self._h = h
 
     @property
@@ -110,25 +112,28 @@ class DeviceVector:
         N.check(N.load().sld_vec_nonzero(self._h, ctypes.byref(out)))
         return bool(out.value)
 
+    def _shape(self, w):
+        return (self.n, w) if self.chains == 1 else (self.chains, self.n, w)
+
     def upload_planes(self, planes):
         p = np.ascontiguousarray(planes, dtype=np.uint64)
-        if p.ndim != 2 or p.shape[0] != self.n:
+        if p.shape[:-1] != self._shape(1)[:-1]:
             raise ValueError("plane count mismatch")
-        N.check(N.load().sld_vec_upload_planes(self._h, N.ptr(p), self.n, p.shape[1]))
+        N.check(N.load().sld_vec_upload_planes(self._h, N.ptr(p), self.n, p.shape[-1]))
 
     def download_planes(self, P):
-        out = np.empty((self.n, P), dtype=np.uint64)
+        out = np.empty(self._shape(P), dtype=np.uint64)
         N.check(N.load().sld_vec_download_planes(self._h, N.ptr(out), self.n, P))
         return out
 
     def upload_limbs(self, limbs):
         a = N.cu32(limbs)
-        if a.shape != (self.n, self.field.L):
-            raise ValueError(f"limb array shape {a.shape} != {(self.n, self.field.L)}")
+        if a.shape != self._shape(self.field.L):
+            raise ValueError(f"limb array shape {a.shape} != {self._shape(self.field.L)}")
         N.check(N.load().sld_vec_upload_limbs(self._h, N.ptr(a), self.n))
 
     def download_limbs(self):
-        out = np.empty((self.n, self.field.L), dtype=np.uint32)
+        out = np.empty(self._shape(self.field.L), dtype=np.uint32)
         N.check(N.load().sld_vec_download_limbs(self._h, N.ptr(out), self.n))
         return out
 
@@ -183,9 +188,9 @@ class DeviceMatrix:
 
     INFO_KEYS = ("nrows", "total_cols", "nnz", "n_pm", "n_small", "n_full", "stripes",
                  "nslices", "device_bytes", "pad_entries", "L", "stride_words", "max_degree",
-                 "stripe_cols")
+                 "stripe_cols", "chains")
 
-    def __init__(self, A, device=None, stripe_cols=0, field=None):
+    def __init__(self, A, device=None, stripe_cols=0, field=None, chains=1):
         self.mod = as_modulus(A.mod)
         self.field = field or Field(self.mod, device)
         self.L = self.field.L
@@ -198,9 +203,10 @@ class DeviceMatrix:
             raise ValueError("row_ptr length must be nrows + 1")
         self.n_dense = n_dense
         self.total_cols = self.ncols + n_dense
+        self.chains = int(chains)
         h = ctypes.c_void_p()
-        N.check(N.load().sld_mat_create(
-            self.field.handle, self.nrows, self.ncols, N.ptr(row_ptr), N.ptr(col), N.ptr(tags),
+        N.check(N.load().sld_mat_create_chains(
+            self.field.handle, self.chains, self.nrows, self.ncols, N.ptr(row_ptr), N.ptr(col), N.ptr(tags),
             N.ptr(small), len(fpos), N.ptr(fpos), N.ptr(flimbs), n_dense,
             N.ptr(dense) if dense is not None else ctypes.c_void_p(0), int(stripe_cols),
             ctypes.byref(h)))
@@ -217,24 +223,29 @@ class DeviceMatrix:
         return {k: int(v) for k, v in zip(self.INFO_KEYS, out)}
 
     def vector(self, n=None):
-        return DeviceVector(self.field, self.total_cols if n is None else n)
+        return DeviceVector(self.field, self.total_cols if n is None else n, self.chains)
 
     def apply_planes(self, planes):
-        """v = A u on digit planes (host in, host out)."""
+        """v = A u on digit planes (host in, host out; chains x n x P when
+        the matrix carries several chains)."""
         p = np.ascontiguousarray(planes, dtype=np.uint64)
-        if p.ndim != 2 or p.shape[0] != self.total_cols:
+        lead = (self.total_cols,) if self.chains == 1 else (self.chains, self.total_cols)
+        if p.shape[:-1] != lead:
             raise ValueError("plane count mismatch")
-        out = np.empty((self.nrows, p.shape[1]), dtype=np.uint64)
-        N.check(N.load().sld_spmv_planes(self._h, N.ptr(p), N.ptr(out), p.shape[1]))
+        out_shape = ((self.nrows,) if self.chains == 1 else (self.chains, self.nrows)) + (p.shape[-1],)
+        out = np.empty(out_shape, dtype=np.uint64)
+        N.check(N.load().sld_spmv_planes(self._h, N.ptr(p), N.ptr(out), p.shape[-1]))
         return out
 
     def spmv(self, vin: DeviceVector, vout: DeviceVector):
         N.check(N.load().sld_spmv(self._h, vin.handle, vout.handle))
 
     def krylov_unit(self, v: DeviceVector, rows, steps):
+        """terms (steps, m, L) -- or (steps, chains, m, L) for several chains."""
         rows = N.c64(rows)
         m = len(rows)
-        terms = np.zeros((int(steps), m, self.L), dtype=np.uint32)
+        shape = (int(steps), m, self.L) if self.chains == 1 else (int(steps), self.chains, m, self.L)
+        terms = np.zeros(shape, dtype=np.uint32)
         N.check(N.load().sld_krylov_unit(self._h, v.handle, N.ptr(rows), m, int(steps),
                                           N.ptr(terms) if terms.size else ctypes.c_void_p(0)))
         return terms

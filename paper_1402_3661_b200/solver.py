@@ -247,6 +247,57 @@ class B200Multiplier:
         return w_planes, verified, horner, tail
 
 
+class B200ChainGroup:
+    """G block-Wiedemann chains advanced together on one B200 (G = 2 or 4):
+    one pass over the matrix serves all G iterates, whose residues sit in
+    one record per column so each gather request fetches G residues.  The
+    chains stay independent (solver.py:220-257); only the memory traffic is
+    shared."""
+
+    def __init__(self, A, chains=2, device=None, stripe_cols=0):
+        if A.nrows != A.ncols + len(getattr(A, "dense_cols", None) or []):
+            raise ValueError("solver needs a square matrix")
+        self.A, self.chains = A, int(chains)
+        self.size, self.mod = int(A.nrows), A.mod
+        self.device = DEFAULT_DEVICE if device is None else int(device)
+        self.stripe_cols = stripe_cols
+        self.count = 0
+        self._dm = None
+        self._vec = None
+        self._lock = threading.Lock()
+
+    @property
+    def dm(self) -> DeviceMatrix:
+        if self._dm is None:
+            self._dm = DeviceMatrix(self.A, self.device, stripe_cols=self.stripe_cols,
+                                    chains=self.chains)
+        return self._dm
+
+    def krylov(self, xblock, v_planes_list, steps):
+        """`steps` steps of the G chains from iterates v_planes_list (G arrays
+        of planes): returns ([terms of chain g] for g < G, [iterate planes])."""
+        if not isinstance(xblock, UnitRows):
+            raise TypeError("chain groups project with UnitRows")
+        G = self.chains
+        if len(v_planes_list) != G:
+            raise ValueError(f"expected {G} iterates")
+        with self._lock:
+            dm = self.dm
+            P = v_planes_list[0].shape[1]
+            if self._vec is None:
+                self._vec = dm.vector()
+            self._vec.upload_planes(np.stack(v_planes_list))
+            terms = dm.krylov_unit(self._vec, xblock.rows, steps)  # (steps, G, m, L)
+            v_out = self._vec.download_planes(P)
+        self.count += int(steps)
+        m = terms.shape[2]
+        out = []
+        for g in range(G):
+            flat = limbs_to_ints(terms[:, g].reshape(-1, terms.shape[3])) if terms.size else []
+            out.append([flat[i * m:(i + 1) * m] for i in range(int(steps))])
+        return out, [v_out[g] for g in range(G)]
+
+
 # the reference's name for the default multiplier
 SequentialMultiplier = B200Multiplier
 
@@ -305,11 +356,17 @@ def _as_planes(vec, mod):
     return ints_to_planes(vec, digit_count(mod.ell))
 
 
-def krylov_block(A, X, Y, count, muls=None, checkpoint=None, contexts=None) -> BlockSequence:
+def krylov_block(A, X, Y, count, muls=None, checkpoint=None, contexts=None,
+                 chains_per_gpu=1) -> BlockSequence:
     """a_i = X^T A^i Y with the n column chains independent
     (solver.py:220-257).  Default multipliers are B200Multipliers spread
-    round-robin over the visible devices; chains run on host threads."""
+    round-robin over the visible devices; chains run on host threads.
+    `chains_per_gpu` = 2 or 4 advances that many chains per matrix pass
+    (B200ChainGroup; unit X, no checkpoint) -- same terms, shared traffic."""
     n = len(Y)
+    if chains_per_gpu > 1 and muls is None and checkpoint is None and isinstance(X, UnitRows) \
+            and n >= chains_per_gpu:
+        return _krylov_block_grouped(A, X, Y, count, chains_per_gpu, contexts)
     if muls is None:
         from ._native import device_count
         ndev = max(1, device_count())
@@ -338,6 +395,37 @@ def krylov_block(A, X, Y, count, muls=None, checkpoint=None, contexts=None) -> B
     m = len(results[0][0][0]) if results and results[0][0] else 0
     return BlockSequence(m=m, n=n, columns=[r[0] for r in results],
                          spmvs_per_column=[r[1] for r in results])
+
+
+def _krylov_block_grouped(A, X, Y, count, G, contexts):
+    from ._native import device_count
+    ndev = max(1, device_count())
+    mod = as_modulus(A.mod)
+    groups = [list(range(k, min(k + G, len(Y)))) for k in range(0, len(Y), G)]
+    if contexts is None:
+        contexts = int(os.environ.get("SLDLAG_CONTEXTS", str(len(groups))))
+
+    def run(gi):
+        idx = groups[gi]
+        planes = [_as_planes(Y[j], mod) for j in idx]
+        if len(idx) < G:  # a short last group runs its chains one by one
+            res = []
+            for j, yp in zip(idx, planes):
+                t, _, _ = krylov_column(B200Multiplier(A, device=gi % ndev), X, yp, count)
+                res.append(t)
+            return res
+        grp = B200ChainGroup(A, chains=G, device=gi % ndev)
+        terms, _ = grp.krylov(X, planes, count)
+        return terms
+
+    if contexts > 1 and len(groups) > 1:
+        with ThreadPoolExecutor(max_workers=contexts) as pool:
+            parts = list(pool.map(run, range(len(groups))))
+    else:
+        parts = [run(g) for g in range(len(groups))]
+    columns = [t for part in parts for t in part]
+    m = len(columns[0][0]) if columns and columns[0] else 0
+    return BlockSequence(m=m, n=len(Y), columns=columns, spmvs_per_column=[count] * len(Y))
 
 
 def krylov_scalar(A, x, y, count=None, mul=None) -> list:
@@ -441,7 +529,7 @@ def draw_blocks(mod, size: int, bp, rng, x_mode="unit", forced_zero=()):
 
 
 __all__ = [
-    "KernelVector", "SolverFailure", "GeneratorFailure", "mksol_block", "mksol_scalar",
+    "B200ChainGroup", "KernelVector", "SolverFailure", "GeneratorFailure", "mksol_block", "mksol_scalar",
     "verify_kernel", "MAX_RESTARTS",
     "BlockingParams", "BlockSequence", "B200Multiplier", "SequentialMultiplier", "UnitRows",
     "DenseRows", "krylov_column", "krylov_block", "krylov_scalar", "krylov_length",

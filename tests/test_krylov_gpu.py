@@ -164,3 +164,37 @@ def test_resume_matches_uninterrupted():
     part, vpart, _ = krylov_column(B200Multiplier(A), X, ints_to_planes(y, P), 23)
     rest, vrest, n = krylov_column(B200Multiplier(A), X, vpart, 50, start_terms=part)
     assert n == 27 and rest == full and np.array_equal(vrest, vfull)
+
+
+@pytest.mark.parametrize("G,bits,stripe", [(2, 200, 0), (4, 200, 0), (2, 480, 0), (2, 200, 37), (4, 127, 50)])
+def test_chain_groups_match_oracle(G, bits, stripe):
+    # G interleaved chains per matrix pass (one gather request per column for
+    # all G residues) give exactly the single-chain sequences
+    from paper_1402_3661_b200 import B200ChainGroup
+    from paper_1402_3661_b200.modring import next_prime
+    mod = PrimeModulus(next_prime(1 << (bits - 1)))
+    rng = np.random.default_rng(G * 1000 + bits + stripe)
+    A = rand_matrix(mod, rng, 160, 158, 11, dense=2)
+    Ys = [mod.random_residues(rng, 160) for _ in range(G)]
+    rows = [0, 77, 159]
+    P = digit_count(mod.ell)
+    grp = B200ChainGroup(A, chains=G, stripe_cols=stripe)
+    terms, vs = grp.krylov(UnitRows(rows), [ints_to_planes(y, P) for y in Ys], 37)
+    orc = to_oracle(A)
+    for g in range(G):
+        ot, ov = O.krylov_unit(orc, O.ints_to_limbs(Ys[g], mod.limbs), rows, 37)
+        assert terms[g] == [O.limbs_to_ints(t) for t in ot], g
+        assert planes_to_ints(vs[g]) == O.limbs_to_ints(ov), g
+    assert grp.count == 37
+
+
+def test_krylov_block_grouped_equals_ungrouped():
+    mod = PrimeModulus(2**200 - 75)
+    rng = np.random.default_rng(31)
+    A = rand_matrix(mod, rng, 90, 90, 8)
+    bp = BlockingParams(5, 10)
+    X, Y = draw_blocks(mod, 90, bp, rng, "unit")
+    one = krylov_block(A, X, Y, 45, contexts=1)
+    two = krylov_block(A, X, Y, 45, chains_per_gpu=2)
+    four = krylov_block(A, X, Y, 45, chains_per_gpu=4)
+    assert one.columns == two.columns == four.columns

@@ -60,3 +60,17 @@ def test_cfg2_krylov_chain_vs_oracle():
     assert n == 12
     assert terms == [O.limbs_to_ints(t) for t in ot]
     assert np.array_equal(planes_to_limbs(v, mod.limbs), ov)
+
+
+def test_cfg2_two_chain_pass_vs_oracle():
+    mod = corpus.random_prime(217, np.random.default_rng(1))
+    A = corpus.generate(corpus.profile_ffs(650_000, seed=1), mod)
+    orc = _oracle(A)
+    u = [_random_residue_limbs(np.random.default_rng(s), A.total_cols, mod) for s in (1, 2)]
+    dm = DeviceMatrix(A, chains=2)
+    vin, vout = dm.vector(), dm.vector()
+    vin.upload_limbs(np.stack(u))
+    dm.spmv(vin, vout)
+    got = vout.download_limbs()
+    for g in range(2):
+        assert np.array_equal(got[g], orc.spmv_limbs(u[g]))

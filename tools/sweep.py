@@ -18,14 +18,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--policies", default="6")
+    ap.add_argument("--policies", default="7")
     ap.add_argument("--stripes", default="0")
     ap.add_argument("--apw", default="0", help="comma list of SLD_APW_RATIO values; 0 = off")
+    ap.add_argument("--chains", default="1", help="comma list of chains per matrix pass")
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
     y = _random_residue_limbs(np.random.default_rng(5), A.total_cols, mod)
-    for sc in [int(x) for x in a.stripes.split(",")]:
+    for G in [int(x) for x in a.chains.split(",")]:
+      for sc in [int(x) for x in a.stripes.split(",")]:
         for pol, apw in [(int(x), float(y)) for x in a.policies.split(",") for y in a.apw.split(",")]:
             os.environ["SLD_POLICY"] = str(pol)
             if apw > 0:
@@ -33,9 +35,9 @@ def main():
                 os.environ["SLD_APW_RATIO"] = str(apw)
             else:
                 os.environ.pop("SLD_APW", None)
-            dm = DeviceMatrix(A, stripe_cols=sc)
+            dm = DeviceMatrix(A, stripe_cols=sc, chains=G)
             v = dm.vector()
-            v.upload_limbs(y)
+            v.upload_limbs(y if G == 1 else np.stack([y] * G))
             dm.bench(v, 10, 0)
             tot, per = dm.bench(v, a.steps, 0)
             tot2, per2 = dm.bench(v, a.steps, 0)
@@ -43,7 +45,8 @@ def main():
             import subprocess
             clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.mem,power.draw,temperature.gpu",
                                   "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
-            print(f"{a.config} stripes={dm.info()['stripes']} policy={pol} apw={apw}: {per:.4f} ms/product  [{clk}]",
+            print(f"{a.config} G={G} stripes={dm.info()['stripes']} policy={pol} apw={apw}: "
+                  f"{per:.4f} ms/pass = {per / G:.4f} ms per chain-product  [{clk}]",
                   flush=True)
             v.close()
             dm.close()
