@@ -33,22 +33,24 @@ METRIC = "SpMV/s mod ℓ (ms per iteration) at 1/2/4/8 B200; % of HBM/IMAD roofl
 
 CONFIGS = {
     # BASELINE.json configs; bp = (n, m) blocking of the block Wiedemann run
-    "cfg1": dict(n=20_000, gamma=20, bits=160, bp=(1, 2), steps=2000, warmup=50,
+    "cfg1": dict(n=20_000, gamma=20, bits=160, bp=(1, 2), steps=2000, warmup=50, chains=1,
                  desc="configs[0]: synthetic N=20K, gamma=20, 160-bit l (CPU-oracle case)"),
-    "cfg2": dict(n=650_000, gamma=100, bits=217, bp=(1, 2), steps=1000, warmup=20,
+    "cfg2": dict(n=650_000, gamma=100, bits=217, bp=(1, 2), steps=1000, warmup=20, chains=2,
                  desc="configs[1]: GF(2^619)-scale N=650K FFS profile, 217-bit l, one sequence"),
-    "cfg3": dict(n=3_600_000, gamma=100, bits=202, bp=(8, 16), steps=400, warmup=10,
+    "cfg3": dict(n=3_600_000, gamma=100, bits=202, bp=(8, 16), steps=400, warmup=10, chains=2,
                  desc="configs[2]: GF(2^809)-scale N=3.6M FFS profile, 202-bit l, "
                       "block Wiedemann (8,16), one sequence per GPU"),
-    "cfg4": dict(n=3_600_000, gamma=100, bits=202, bp=(1, 2), steps=100, warmup=5,
+    "cfg4": dict(n=3_600_000, gamma=100, bits=202, bp=(1, 2), steps=100, warmup=5, chains=1,
                  desc="configs[3]: the cfg3 matrix, ONE sequence row/2D-partitioned over the GPUs "
                       "(grid r x c, NCCL exchange)"),
-    "cfg5": dict(n=1_000_000, gamma=100, bits=650, bp=(8, 16), steps=200, warmup=10,
+    "cfg5": dict(n=1_000_000, gamma=100, bits=650, bp=(8, 16), steps=200, warmup=10, chains=1,
                  desc="configs[4]: wide-prime stress N=1M FFS profile, 650-bit l, one sequence per GPU"),
 }
 DEFAULT_CONFIG = "cfg3"
 
-L2_GATHER_PEAK_GBS = 9200.0  # measured random 32-byte L2 gather rate, profiles/microbench_r01.txt
+# measured random-gather rates from L2 (GB/s) for records of 1, 2, 4 sectors
+# fetched by one request (profiles/microbench_r01.txt, microbench2_r01.txt)
+L2_GATHER_PEAK_GBS = {1: 9200.0, 2: 15460.0, 4: 15000.0}
 
 
 def dist_env():
@@ -320,6 +322,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--grid", default=None, help="cfg4 grid RxC (default: <gpus>x1)")
+    ap.add_argument("--chains", type=int, default=None,
+                    help="Krylov chains advanced per matrix pass on each GPU (1, 2, 4)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     args.steps = args.steps or cfg["steps"]
@@ -358,14 +362,17 @@ def main():
     _native.load()
     A, wit, mod = build_matrix(cfg, log)
     t = time.time()
-    dm = DeviceMatrix(A, device=local)
+    G = args.chains or cfg["chains"]
+    G = min(G, 4 if mod.limbs <= 8 else (2 if mod.limbs <= 16 else 1))
+    dm = DeviceMatrix(A, device=local, chains=G)
     info = dm.info()
     log(f"device layout built in {time.time() - t:.1f}s: {info}")
     L, P = dm.L, digit_count(mod.ell)
     rng = np.random.default_rng(1000 + rank)
-    y = _random_residue_limbs(rng, A.total_cols, mod)
+    ys = [_random_residue_limbs(rng, A.total_cols, mod) for _ in range(G)]
+    y = ys[0]
     v = dm.vector()
-    v.upload_limbs(y)
+    v.upload_limbs(ys[0] if G == 1 else np.stack(ys))
 
     # ---- device-timed region: W untimed, then exactly K products
     dm.bench(v, args.warmup, 0)
@@ -381,35 +388,47 @@ def main():
         total_ms = max_over_ranks(dist, total_ms, local)
         dist.barrier()
     steps_even = 2 * ((args.steps + 1) // 2)  # the bench graph replays product pairs
-    ms_per_step = total_ms / steps_even
-    value = world * steps_even / (total_ms / 1e3)
+    ms_per_step = total_ms / steps_even       # one step = one product of each of the G chains
+    value = world * G * steps_even / (total_ms / 1e3)
     launches = steps_even * info["stripes"]
 
-    # ---- end to end through the public API: krylov_column with host y in,
-    # host terms (m per step) and the final iterate out
+    # ---- end to end through the public API with host y in, host terms (m
+    # per chain and step) and the final iterates out: krylov_column for one
+    # chain, the chain group (what krylov_block(chains_per_gpu=G) runs) for G
     bp_m = cfg["bp"][1]
     X = UnitRows(sorted(int(r) for r in np.random.default_rng(7).choice(A.nrows, bp_m, replace=False)))
-    y_planes = limbs_to_planes(y, P)
-    mul = B200Multiplier(A, device=local, dm=dm)
+    y_planes = [limbs_to_planes(yy, P) for yy in ys]
+    if G == 1:
+        mul = B200Multiplier(A, device=local, dm=dm)
+        api = "krylov_column(B200Multiplier, UnitRows)"
+    else:
+        from paper_1402_3661_b200 import B200ChainGroup
+        mul = B200ChainGroup(A, chains=G, device=local)
+        mul._dm = dm
+        api = f"B200ChainGroup(chains={G}).krylov(UnitRows) [krylov_block(chains_per_gpu={G})]"
     e2e_steps = args.steps
     if dist is not None:
         dist.barrier()
     with ClockSampler(local) as clk_e2e:
         t0 = time.perf_counter()
-        terms, v_out, spmvs = krylov_column(mul, X, y_planes, e2e_steps)
+        if G == 1:
+            terms, v_out, spmvs = krylov_column(mul, X, y_planes[0], e2e_steps)
+            v_bytes = v_out.nbytes
+        else:
+            terms, v_outs = mul.krylov(X, y_planes, e2e_steps)
+            v_bytes = sum(vv.nbytes for vv in v_outs)
         t_e2e = time.perf_counter() - t0
     if dist is not None:
-        import torch
         t_e2e = max_over_ranks(dist, t_e2e, local)
-    e2e_value = world * e2e_steps / t_e2e
-    h2d = y_planes.nbytes + 8 * bp_m
-    d2h = e2e_steps * bp_m * 4 * L + v_out.nbytes
+    e2e_value = world * G * e2e_steps / t_e2e
+    h2d = sum(yp.nbytes for yp in y_planes) + 8 * bp_m
+    d2h = e2e_steps * G * bp_m * 4 * L + v_bytes
     # the plain multiplier protocol as well: host planes in/out every product
     n_apply = 3 if A.nrows > 1_000_000 else 10
+    pl = y_planes[0] if G == 1 else np.stack(y_planes)
     t0 = time.perf_counter()
-    pl = y_planes
     for _ in range(n_apply):
-        pl = mul.apply(pl)
+        pl = dm.apply_planes(pl)
     t_apply = time.perf_counter() - t0
 
     # ---- kernel correctness spot check at full size: planted witness A w = 0
@@ -419,38 +438,46 @@ def main():
         wv = [0] * A.total_cols
         for c, val in wit[0].items():
             wv[c] = val
-        ok_witness = not any(planes_to_ints(dm.apply_planes(ints_to_planes(wv, P))))
+        wp = ints_to_planes(wv, P)
+        out = dm.apply_planes(wp if G == 1 else np.stack([wp] * G))
+        ok_witness = not any(planes_to_ints(out.reshape(-1, P)))
 
-    # ---- roofline (SURVEY.md 8(d) algorithmic bytes per product)
+    # ---- roofline (SURVEY.md 8(d) algorithmic bytes per product; the index
+    # stream is read once per pass for all G chains)
     B, Z, Zs, Zf = algorithmic_bytes(A, L)
+    W = 4 * L
+    B_pass = B + (G - 1) * (W * Zf + 2 * A.nrows * W)
     peak, peak_kind = measured_peaks()
-    achieved = B / (ms_per_step / 1e3) / 1e9
+    achieved = B_pass / (ms_per_step / 1e3) / 1e9
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}_g{G}.json")
     if os.path.exists(tfile):
         with open(tfile) as f:
-            traffic = json.load(f).get("dram_bytes_per_product")
-    gather_bytes = 32 * ((4 * L + 31) // 32) * (Z + Zf) + B
+            traffic = json.load(f).get("dram_bytes_per_pass")
+    gather_bytes = G * 32 * ((4 * L + 31) // 32) * (Z + Zf) + B_pass
+    gpeak = L2_GATHER_PEAK_GBS[G]
     line = {
         "metric": METRIC, "value": value, "unit": "SpMV/s", "n_gpus": world, "steps": steps_even,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 limbs, exact mod l (int64 lazy accumulation)",
         "data": "synthetic (native corpus generator, FFS profile, seed 1, planted kernel column)",
-        "config": config_block(args.config, cfg, A, mod, world),
+        "config": dict(config_block(args.config, cfg, A, mod, world), chains_per_gpu=G,
+                       step=f"one product of each of the {G} chain(s) on every GPU"),
+        "ms_per_chain_product": ms_per_step / G,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_product": B, "kernel": "spmv_pass (all stripe passes)"},
-        "gather_roofline": {"bound": "l2_random_sector_gather", "peak": L2_GATHER_PEAK_GBS,
-                            "unit": "GB/s", "bytes_per_product": gather_bytes,
+                     "algorithmic_bytes_per_step": B_pass, "algorithmic_bytes_per_product": B,
+                     "kernel": "spmv_pass (all stripe passes of one step)"},
+        "gather_roofline": {"bound": "l2_random_gather_requests", "peak": gpeak,
+                            "unit": "GB/s", "bytes_per_step": gather_bytes,
                             "achieved": gather_bytes / (ms_per_step / 1e3) / 1e9,
-                            "frac": gather_bytes / (ms_per_step / 1e3) / 1e9 / L2_GATHER_PEAK_GBS},
+                            "frac": gather_bytes / (ms_per_step / 1e3) / 1e9 / gpeak},
         "int_ops_per_product": int_ops(A, L),
         "e2e": {"value": e2e_value, "unit": "SpMV/s", "h2d_bytes_per_step": h2d / e2e_steps,
-                "d2h_bytes_per_step": d2h / e2e_steps, "api": "krylov_column(B200Multiplier, UnitRows)",
-                "steps": e2e_steps},
-        "e2e_apply": {"value": world * n_apply / t_apply, "unit": "SpMV/s",
-                      "h2d_bytes_per_step": y_planes.nbytes, "d2h_bytes_per_step": y_planes.nbytes,
-                      "api": "B200Multiplier.apply(planes) per product"},
+                "d2h_bytes_per_step": d2h / e2e_steps, "api": api, "steps": e2e_steps},
+        "e2e_apply": {"value": world * G * n_apply / t_apply, "unit": "SpMV/s",
+                      "h2d_bytes_per_step": G * y_planes[0].nbytes, "d2h_bytes_per_step": G * y_planes[0].nbytes,
+                      "api": "DeviceMatrix.apply_planes (the multiplier's apply) per product"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "clocks_e2e": clk_e2e.summary(),

@@ -19,13 +19,15 @@ def main():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--stripe-cols", type=int, default=0)
+    ap.add_argument("--chains", type=int, default=1)
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
-    dm = DeviceMatrix(A, stripe_cols=a.stripe_cols)
+    dm = DeviceMatrix(A, stripe_cols=a.stripe_cols, chains=a.chains)
     print(dm.info(), file=sys.stderr)
     v = dm.vector()
-    v.upload_limbs(_random_residue_limbs(np.random.default_rng(5), A.total_cols, mod))
+    y = _random_residue_limbs(np.random.default_rng(5), A.total_cols, mod)
+    v.upload_limbs(y if a.chains == 1 else np.stack([y] * a.chains))
     tot, per = dm.bench(v, a.steps, 0)
     print(f"{a.steps} products: {per:.4f} ms/product (stripes={dm.info()['stripes']})", file=sys.stderr)
 
