@@ -51,6 +51,11 @@ typedef struct sld_vec sld_vec;
 int sld_version(void);
 const char *sld_last_error(void);
 int sld_device_count(int *out);
+/* Which die each SM of `device` sits on (B200 is two dies, and each die's
+ * L2 caches what its own SMs read).  map256[smid] = 0/1; n_die0/n_die1 = SMs
+ * per die.  Probed once per device and process from cold-line latencies.
+ * Returns SLD_E_CUDA (map all zero) when the probe is ambiguous. */
+int sld_die_map(int device, uint8_t *map256, int *n_die0, int *n_die1);
 
 /*
  * Field context: one prime l on one device.  Replaces PrimeModulus as the
@@ -102,7 +107,8 @@ int sld_mat_create_chains(sld_ctx *ctx, int chains, int64_t nrows, int64_t ncols
 int sld_mat_destroy(sld_mat *m);
 /* info[0..15]: nrows, total_cols, nnz, n_pm, n_small, n_full(+dense nz),
  * stripes, nslices, device bytes, padded index entries, L, stride words,
- * max row degree, stripe columns, chains, 0 */
+ * max row degree, stripe columns, chains, halves (2 = columns dealt to
+ * the two dies, see sld_die_map) */
 int sld_mat_info(const sld_mat *m, int64_t *info);
 
 /*

@@ -22,7 +22,7 @@ SLD_E_NCCL = -4
 
 # every symbol include/sldb200.h declares (checked by tests/test_native_abi.py)
 EXPORTS = [
-    "sld_version", "sld_last_error", "sld_device_count",
+    "sld_version", "sld_last_error", "sld_device_count", "sld_die_map",
     "sld_ctx_create", "sld_ctx_destroy", "sld_ctx_sync", "sld_ctx_set_stream", "sld_add_mod",
     "sld_vec_read_rows", "sld_lincomb", "sld_vec_nonzero",
     "sld_mat_create", "sld_mat_create_chains", "sld_mat_destroy", "sld_mat_info",
@@ -67,6 +67,7 @@ def load(build_if_missing=False):
             "sld_version": ([], i32),
             "sld_last_error": ([], ctypes.c_char_p),
             "sld_device_count": ([vp], i32),
+            "sld_die_map": ([i32, vp, vp, vp], i32),
             "sld_ctx_create": ([i32, vp, i32, pp], i32),
             "sld_ctx_destroy": ([vp], i32),
             "sld_ctx_sync": ([vp], i32),
@@ -124,6 +125,18 @@ def device_count():
     if rc != SLD_OK:
         return 0
     return n.value
+
+
+def die_map(device=0):
+    """(map[256] of %smid -> die, SMs on die 0, SMs on die 1), or None when
+    the probe is ambiguous (the SpMV then runs without the die split)."""
+    import numpy as np
+    m = np.zeros(256, dtype=np.uint8)
+    n0, n1 = ctypes.c_int(0), ctypes.c_int(0)
+    rc = load().sld_die_map(int(device), m.ctypes.data, ctypes.byref(n0), ctypes.byref(n1))
+    if rc != SLD_OK:
+        return None
+    return m, n0.value, n1.value
 
 
 def ptr(a):

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <string>
 #include <thread>
@@ -128,6 +129,8 @@ struct sld_ctx {
   void* dstage = nullptr;  // device staging (limb format)
   size_t dstage_bytes = 0;
   size_t apw_max = 0;      // max access-policy window bytes (0: unsupported)
+  uint8_t* die_map = nullptr;  // device copy of the %smid -> die map (256 entries)
+  int die_n[2] = {0, 0};       // SMs per die; both 0 if the map is unavailable
 };
 
 struct sld_vec {
@@ -172,6 +175,13 @@ struct sld_mat {
   uint32_t* full_val = nullptr;
   uint32_t* dense_val = nullptr;
   uint32_t* part = nullptr;  // slot-indexed partials (npass > 1)
+  // die split (halves == 2): each pass's columns are dealt to the two dies
+  int halves = 1;
+  int64_t half_chunk = 0;      // columns per interleaved chunk
+  unsigned split_grid = 0;     // persistent CTAs of the split kernel
+  uint32_t* xch = nullptr;     // [2][nslots * G * SW]
+  uint32_t* cnt = nullptr;     // [nslices] arrival counters
+  uint32_t* queue = nullptr;   // [4] work queues + exit counter
   // host-planes convenience staging
   uint64_t* stage = nullptr;
   size_t stage_bytes = 0;
@@ -200,6 +210,146 @@ static const LOps& ops(int L) {
   }();
   (void)init;
   return table[L];
+}
+
+// ------------------------------------------------------------ die map
+//
+// Which of B200's two dies each SM sits on (yield-dependent, so probed per
+// device): a cold line's first load costs ~590 cycles from an SM on the die
+// whose HBM holds it and ~970 from the other die (profiles/microbench3_r01.txt).
+// Probe lines are dropped from L2 with discard.global.L2, then the SM under
+// test times its first load of each; SMs of one die agree on the near/far
+// pattern, the two dies see complementary patterns.  An ambiguous result
+// disables the die split (the plain stripe passes still run on the GPU).
+
+namespace {
+constexpr int DIE_PROBES = 64;
+constexpr int DIE_STRIDE = 1056;  // words between probe lines (> 2 KB apart)
+
+__global__ void die_nsmid(int* out) {
+  uint32_t n;
+  asm volatile("mov.u32 %0, %%nsmid;" : "=r"(n));
+  *out = (int)n;
+}
+__global__ void die_discard(uint32_t* buf) {
+  const int i = threadIdx.x;
+  if (i < DIE_PROBES) asm volatile("discard.global.L2 [%0], 128;" ::"l"(buf + (size_t)i * DIE_STRIDE) : "memory");
+}
+__global__ void die_time(const uint32_t* buf, int target, uint32_t* lat, int* hit) {
+  if (sm_id() != (uint32_t)target || threadIdx.x != 0) return;
+  if (atomicExch(hit, 1) != 0) return;
+  uint32_t dep = 0;
+  for (int i = 0; i < DIE_PROBES; i++) {
+    const uint32_t* p = buf + (size_t)i * DIE_STRIDE + dep;
+    uint64_t t0, t1;
+    uint32_t v;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0) : "r"(dep) : "memory");
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    dep = v >> 31 & 0u;  // 0, but the clock read below waits for the load
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1) : "r"(v) : "memory");
+    lat[i] = (uint32_t)(t1 - t0);
+  }
+}
+
+struct DieMap {
+  bool probed = false;
+  bool ok = false;
+  uint8_t map[256] = {0};
+  int n[2] = {0, 0};
+  std::string why;
+};
+std::mutex g_die_mu;
+DieMap g_die[64];
+
+int probe_dies(int dev, DieMap& d, int sms) {
+  uint32_t *buf = nullptr, *lat = nullptr;
+  int *hit = nullptr, *nsm = nullptr;
+  const int T = 256;
+  CU(cudaMalloc(&buf, (size_t)DIE_PROBES * DIE_STRIDE * 4 + 256));
+  CU(cudaMalloc(&lat, (size_t)T * DIE_PROBES * 4));
+  CU(cudaMalloc(&hit, T * 4));
+  CU(cudaMalloc(&nsm, 4));
+  CU(cudaMemset(buf, 0, (size_t)DIE_PROBES * DIE_STRIDE * 4 + 256));
+  CU(cudaMemset(hit, 0, T * 4));
+  die_nsmid<<<1, 1>>>(nsm);
+  int nsmid = 0;
+  CU(cudaMemcpy(&nsmid, nsm, 4, cudaMemcpyDeviceToHost));
+  nsmid = std::min(std::max(nsmid, sms), T);
+  for (int t = 0; t < nsmid; t++) {
+    die_discard<<<1, DIE_PROBES>>>(buf);
+    die_time<<<sms * 4, 32>>>(buf, t, lat + (size_t)t * DIE_PROBES, hit + t);
+  }
+  std::vector<uint32_t> L((size_t)T * DIE_PROBES);
+  std::vector<int> H(T);
+  CU(cudaMemcpy(L.data(), lat, L.size() * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(H.data(), hit, T * 4, cudaMemcpyDeviceToHost));
+  cudaFree(buf);
+  cudaFree(lat);
+  cudaFree(hit);
+  cudaFree(nsm);
+  // near/far pattern of each SM against its own midpoint
+  std::vector<uint8_t> ref;
+  d.ok = true;
+  for (int t = 0; t < nsmid && d.ok; t++) {
+    if (!H[t]) continue;
+    const uint32_t* l = &L[(size_t)t * DIE_PROBES];
+    const uint32_t lo = *std::min_element(l, l + DIE_PROBES), hi = *std::max_element(l, l + DIE_PROBES);
+    if (hi - lo < 150) {
+      d.ok = false;
+      d.why = "no near/far latency split on sm " + std::to_string(t);
+      break;
+    }
+    std::vector<uint8_t> near(DIE_PROBES);
+    for (int i = 0; i < DIE_PROBES; i++) near[i] = l[i] * 2 < lo + hi;
+    if (ref.empty()) ref = near;
+    int agree = 0;
+    for (int i = 0; i < DIE_PROBES; i++) agree += near[i] == ref[i];
+    if (agree >= DIE_PROBES * 9 / 10) d.map[t] = 0;
+    else if (agree <= DIE_PROBES / 10) d.map[t] = 1;
+    else {
+      d.ok = false;
+      d.why = "ambiguous near/far pattern on sm " + std::to_string(t);
+      break;
+    }
+    d.n[d.map[t]]++;
+  }
+  if (d.ok && (d.n[0] == 0 || d.n[1] == 0)) {
+    d.ok = false;
+    d.why = "all SMs on one die";
+  }
+  if (!d.ok) memset(d.map, 0, sizeof(d.map));
+  (void)dev;
+  return SLD_OK;
+}
+}  // namespace
+
+static const DieMap* die_map(int dev, int sms) {
+  std::lock_guard<std::mutex> g(g_die_mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  DieMap& d = g_die[dev];
+  if (!d.probed) {
+    d.probed = true;
+    if (probe_dies(dev, d, sms) != SLD_OK) {
+      d.ok = false;
+      d.why = "probe failed: " + g_err;
+    }
+  }
+  return &d;
+}
+
+extern "C" int sld_die_map(int device, uint8_t* map256, int* n_die0, int* n_die1) {
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(SLD_E_ARG, "device %d out of range (%d)", device, ndev);
+  CU(cudaSetDevice(device));
+  cudaDeviceProp pr;
+  CU(cudaGetDeviceProperties(&pr, device));
+  const DieMap* d = die_map(device, pr.multiProcessorCount);
+  if (map256) memcpy(map256, d->map, 256);
+  if (n_die0) *n_die0 = d->n[0];
+  if (n_die1) *n_die1 = d->n[1];
+  if (!d->ok) return fail(SLD_E_CUDA, "die map unavailable: %s", d->why.c_str());
+  return SLD_OK;
 }
 
 // ------------------------------------------------------------- context
@@ -282,6 +432,15 @@ extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pr.persistingL2CacheMaxSize);
   CU(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
+  {
+    const DieMap* d = die_map(device, c->sms);
+    CU(cudaMalloc(&c->die_map, 256));
+    CU(cudaMemcpy(c->die_map, d->map, 256, cudaMemcpyHostToDevice));
+    if (d->ok) {
+      c->die_n[0] = d->n[0];
+      c->die_n[1] = d->n[1];
+    }
+  }
   *out = c.release();
   return SLD_OK;
 }
@@ -290,6 +449,7 @@ extern "C" int sld_ctx_destroy(sld_ctx* c) {
   if (!c) return SLD_OK;
   cudaSetDevice(c->dev);
   if (c->own) cudaStreamDestroy(c->own);
+  if (c->die_map) cudaFree(c->die_map);
   if (c->hstage) cudaFreeHost(c->hstage);
   if (c->dstage) cudaFree(c->dstage);
   delete c;
@@ -635,7 +795,7 @@ static void mat_free(sld_mat* m) {
   if (!m) return;
   void* ptrs[] = {m->slices, m->pm_idx, m->s_idx, m->s_coef, m->slot_row, m->lane_k4, m->full_ptr,
                   m->full_col, m->full_val, m->dense_val, m->part, m->stage, m->proj_rows,
-                  m->terms_dev, m->dproj_part};
+                  m->terms_dev, m->dproj_part, m->xch, m->cnt, m->queue};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->tmp_in) sld_vec_destroy(m->tmp_in);
@@ -684,17 +844,35 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
       return fail(SLD_E_ARG, "full positions must be sorted and in range");
     if (tags[full_pos[k]] != 3) return fail(SLD_E_ARG, "full position without full tag");
   }
-  // ---- stripes: keep the gathered column window L2-resident
+  // ---- die split and stripes: keep each pass's gathered columns L2-resident
+  const double vec_bytes = (double)(M->total_cols + 1) * SW * 4.0 * M->chains;
+  const double l2 = (double)c->l2_bytes;
+  int H = 1;
+  {
+    // measured (tools/microbench/mb3.cu): with every SM gathering every
+    // column the L2 holds ~one die's worth (~63 MB); dealing the columns to
+    // the dies keeps ~128 MB resident.  Split once the vector outgrows ~0.4 L2.
+    int want = vec_bytes > 0.4 * l2 ? 1 : 0;
+    if (const char* e = getenv("SLD_SPLIT")) want = atoi(e);
+    if (want && c->die_n[0] > 0 && c->die_n[1] > 0 && nrows > 0 &&
+        ops(L).split_occupancy(M->chains) > 0)
+      H = 2;
+  }
   int64_t stripe = max_stripe_cols;
   if (stripe <= 0) {
-    // measured (tools/sweep.py): one pass while the gathered vector fits in
-    // ~80% of L2 (cfg2 21 MB, cfg5 96 MB); beyond that, stripes of <= 1/2 L2
-    // (cfg3: 2 x 58 MB) so each pass's working set stays L2-resident
-    const double vec_bytes = (double)(M->total_cols + 1) * SW * 4.0 * M->chains;
-    if (vec_bytes <= 0.80 * (double)c->l2_bytes) {
+    // measured (tools/sweep.py): without the split, one pass while the
+    // gathered vector fits in ~80% of L2 (cfg2 21 MB, cfg5 96 MB), beyond that
+    // stripes of <= 1/2 L2 (cfg3: 2 x 58 MB).  With the split, stripes of
+    // <= SLD_SPLIT_FRAC (default 0.95) of L2.
+    double frac_one = 0.80, frac_many = 0.5;
+    if (H == 2) {
+      frac_one = frac_many = 0.95;
+      if (const char* e = getenv("SLD_SPLIT_FRAC")) frac_one = frac_many = atof(e);
+    }
+    if (vec_bytes <= frac_one * l2) {
       stripe = ncols;
     } else {
-      const int64_t parts = (int64_t)std::ceil(vec_bytes / (0.5 * (double)c->l2_bytes));
+      const int64_t parts = (int64_t)std::ceil(vec_bytes / (frac_many * l2));
       stripe = (ncols + parts - 1) / parts;
     }
     stripe = std::max<int64_t>(1, stripe);
@@ -703,10 +881,27 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   const int npass = (int)std::max<int64_t>(1, (ncols + stripe - 1) / stripe);
   M->npass = npass;
   M->stripe_cols = stripe;
+  M->halves = H;
+  // interleaved chunks of >= 2 KB of whole 128-byte lines, dealt to the dies
+  // in proportion to their SM counts (Bresenham), so both the bytes each
+  // die's L2 must hold and the gathers each die serves follow its SM share
+  const int64_t rec_bytes = (int64_t)SW * 4 * M->chains;
+  int64_t line_recs = 1;
+  while ((line_recs * rec_bytes) % 128) line_recs++;
+  const int64_t HC = line_recs * std::max<int64_t>(1, (2048 + line_recs * rec_bytes - 1) / (line_recs * rec_bytes));
+  M->half_chunk = HC;
+  const int64_t dn0 = c->die_n[0], dn = c->die_n[0] + c->die_n[1];
+  auto half_of = [&](int64_t col) -> int {
+    if (H == 1) return 0;
+    const int64_t k = col / HC;
+    return (((k + 1) * dn0) / dn - (k * dn0) / dn) ? 0 : 1;
+  };
+  auto part_of = [&](int64_t col) -> int { return (int)(col / stripe) * H + half_of(col); };
+  const int npart = npass * H;
   // ---- per-row, per-pass class counts
   RowCounts rc;
-  rc.pm.assign((size_t)npass * nrows, 0);
-  rc.sm.assign((size_t)npass * nrows, 0);
+  rc.pm.assign((size_t)npart * nrows, 0);
+  rc.sm.assign((size_t)npart * nrows, 0);
   std::vector<uint32_t> fcount(nrows + 1, 0);
   // map flat position -> full value index (only for tag 3); sorted positions
   std::atomic<int> bound_bad{0};
@@ -715,7 +910,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
       uint32_t tot_s = 0, tot_pm = 0, nf = 0;
       for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; p++) {
         const int t = tags[p];
-        const int pass = (int)(col_idx[p] / stripe);
+        const int pass = part_of(col_idx[p]);
         if (t <= 1) {
           rc.pm[(size_t)pass * nrows + r]++;
           tot_pm++;
@@ -744,7 +939,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   parallel_for(nrows, [&](int64_t lo, int64_t hi) {
     for (int64_t r = lo; r < hi; r++) {
       int64_t a = 0, b = 0;
-      for (int p = 0; p < npass; p++) {
+      for (int p = 0; p < npart; p++) {
         a += rc.pm[(size_t)p * nrows + r];
         b += rc.sm[(size_t)p * nrows + r];
       }
@@ -770,9 +965,9 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   std::vector<int32_t> slot_row(nslots, -1);
   for (int64_t s = 0; s < nrows; s++) slot_row[s] = order[s];
   // ---- slice tables
-  std::vector<SliceInfo> slices((size_t)npass * nslices);
+  std::vector<SliceInfo> slices((size_t)npart * nslices);
   uint64_t pm_units = 0, s_units = 0;
-  for (int p = 0; p < npass; p++) {
+  for (int p = 0; p < npart; p++) {
     for (int64_t s = 0; s < nslices; s++) {
       uint32_t kpm = 0, ks = 0;
       for (int l = 0; l < RH; l++) {
@@ -793,10 +988,10 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     }
   }
   // per-lane group counts (the SELL slice width is only the max over lanes)
-  std::vector<uint32_t> lane_k4((size_t)npass * nslots, 0);
+  std::vector<uint32_t> lane_k4((size_t)npart * nslots, 0);
   if (std::max(gamma_pm_max, gamma_s_max) >= (1u << 18))
     return fail(SLD_E_BOUND, "row too long for the per-lane group counter");
-  for (int p = 0; p < npass; p++)
+  for (int p = 0; p < npart; p++)
     for (int64_t slot = 0; slot < nrows; slot++) {
       const int32_t r = slot_row[slot];
       const uint32_t a = (rc.pm[(size_t)p * nrows + r] + 3) / 4, b = (rc.sm[(size_t)p * nrows + r] + 3) / 4;
@@ -817,7 +1012,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   std::vector<uint32_t> full_val((size_t)nf_total * SW, 0);
   std::atomic<int64_t> pads{0};
   parallel_for(nslots, [&](int64_t lo, int64_t hi) {
-    std::vector<uint32_t> kp(npass), ks(npass);
+    std::vector<uint32_t> kp(npart), ks(npart);
     int64_t mypads = 0;
     for (int64_t slot = lo; slot < hi; slot++) {
       const int32_t r = slot_row[slot];
@@ -830,7 +1025,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
       for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; p++) {
         const int t = tags[p];
         const uint32_t col = (uint32_t)col_idx[p];
-        const int pass = (int)(col_idx[p] / stripe);
+        const int pass = part_of(col_idx[p]);
         const SliceInfo& si = slices[(size_t)pass * nslices + slice];
         if (t <= 1) {
           const uint32_t k = kp[pass]++;
@@ -871,9 +1066,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
           for (int i = 0; i < L; i++) dst[i] = full_limbs[(size_t)fi * L + i];
         full_col[fk++] = col;
       }
-      for (int q = 0; q < npass; q++) {
-        const SliceInfo& si = slices[(size_t)q * nslices + slice];
-        (void)si;
+      for (int q = 0; q < npart; q++) {
         mypads += (int64_t)((kp[q] + 3) / 4) * 4 - kp[q] + (int64_t)((ks[q] + 3) / 4) * 4 - ks[q];
       }
     }
@@ -932,6 +1125,18 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     CU(cudaMalloc(&M->part, (size_t)nslots * M->chains * SW * 4));
     acct += (size_t)nslots * M->chains * SW * 4;
   }
+  if (H == 2) {
+    const size_t xb = (size_t)2 * nslots * M->chains * SW * 4;
+    CU(cudaMalloc(&M->xch, xb));
+    CU(cudaMalloc(&M->cnt, std::max<size_t>((size_t)nslices * 4, 16)));
+    CU(cudaMemset(M->cnt, 0, std::max<size_t>((size_t)nslices * 4, 16)));
+    CU(cudaMalloc(&M->queue, 16));
+    CU(cudaMemset(M->queue, 0, 16));
+    acct += xb + (size_t)nslices * 4 + 16;
+    int occ = ops(L).split_occupancy(M->chains);
+    if (const char* e = getenv("SLD_SPLIT_OCC")) occ = std::max(1, std::min(occ, atoi(e)));
+    M->split_grid = (unsigned)(occ * c->sms);
+  }
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(c->stream));
   M->dev_bytes = acct;
@@ -982,7 +1187,7 @@ extern "C" int sld_mat_info(const sld_mat* m, int64_t* info) {
   if (!m || !info) return fail(SLD_E_ARG, "null argument");
   int64_t v[16] = {m->nrows, m->total_cols, m->nnz, m->n_pm, m->n_small, m->n_full,
                    m->npass, m->nslices, (int64_t)m->dev_bytes, m->pad_entries,
-                   m->ctx->L, m->ctx->SW, m->max_deg, m->stripe_cols, m->chains, 0};
+                   m->ctx->L, m->ctx->SW, m->max_deg, m->stripe_cols, m->chains, m->halves};
   memcpy(info, v, sizeof(v));
   return SLD_OK;
 }
@@ -1024,6 +1229,18 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
       a.slices = M->slices;
       a.lane_k4 = M->lane_k4;
       o.pass(M->chains, 1, 1, 1, c->stream, a, c->mp);
+    }
+    return;
+  }
+  if (M->halves == 2) {
+    a.die_map = c->die_map;
+    a.xch = M->xch;
+    a.cnt = M->cnt;
+    a.queue = M->queue;
+    for (int p = 0; p < M->npass; p++) {
+      a.slices = M->slices + (size_t)p * 2 * M->nslices;
+      a.lane_k4 = M->lane_k4 + (size_t)p * 2 * M->nslots;
+      o.split(M->chains, p == 0, p == M->npass - 1, M->split_grid, c->stream, a, c->mp);
     }
     return;
   }

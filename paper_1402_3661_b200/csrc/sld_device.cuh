@@ -63,6 +63,12 @@ struct SpmvArgs {
   int has_full;
   int policy;  // bit0 gather L2 evict_last, bit1 output store evict_first,
                // bit2 partial store evict_first, bit3 gathers L1::no_allocate
+  // die-split passes (spmv_split): slices / lane_k4 hold both halves, half h
+  // at offset h * nslices / h * nslots
+  const uint8_t* die_map;  // %smid -> die (0/1)
+  uint32_t* xch;           // [2][nslots * G * SW] the halves' row values
+  uint32_t* cnt;           // [nslices] arrival counters (parity = order)
+  uint32_t* queue;         // [3] work queue per die + exit counter
 };
 
 // ---------------------------------------------------------------- loads
@@ -296,41 +302,16 @@ __host__ __device__ constexpr int spmv_batch() { return L <= 8 ? 4 : (L <= 16 ? 
 // which the L1 coalesces into ONE request.  Random gathers are request-bound
 // (~1 sector-request per SM per clock, profiles/microbench2_r01.txt), so a
 // 2-sector record moves ~1.7x the useful bytes per second of a 1-sector one.
-template <int L, int G, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const SpmvArgs a, const ModParams mp) {
+
+// the +-1 and small entries of one row in one part (column stripe [x half])
+template <int L, int G>
+__device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& si, uint32_t kk, int rw,
+                                            const uint32_t* xc, uint64_t pol, uint64_t gpol,
+                                            int64_t (&acc)[L + 1], int64_t& S) {
   constexpr int SW = stride_words(L);
   constexpr int NB = spmv_batch<L>();
-  constexpr int R = 32 / G;  // rows per warp = slice height
-  const int lane = threadIdx.x & 31;
-  const int chain = lane & (G - 1);
-  const int rw = lane / G;
-  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t slot = slice * R + rw;
-
-  if (FIRST && blockIdx.x == 0 && threadIdx.x < a.proj_m * G) {
-    // a_i = X^T v_i of the iterate this product consumes (solver.py:210)
-    const int t = threadIdx.x / G, c = threadIdx.x % G;
-    const uint32_t* src = a.x + ((size_t)a.proj_rows[t] * G + c) * SW;
-    uint32_t* dst = a.terms_out + ((size_t)t * G + c) * SW;
-#pragma unroll
-    for (int i = 0; i < SW; i++) dst[i] = i < L ? (src[i] ^ 0x80000000u) : 0u;
-  }
-  if (slice >= a.nslices) return;
-
-  const uint64_t pol = policy_evict_first();
-  const uint64_t gpol = (a.policy & 1) ? policy_evict_last() : createpolicy_normal();
-  const SliceInfo si = a.slices[slice];
-  // per-row group counts: lanes stop at their own row length, so padded
-  // SELL positions are never loaded (no index or gather traffic)
-  const uint32_t kk = a.lane_k4[slot];
+  constexpr int R = 32 / G;
   const uint32_t my_pm = kk & 0xFFFFu, my_s = kk >> 16;
-  const uint32_t* xc = a.x + (size_t)chain * SW;  // this lane's chain in every record
-  int64_t acc[L + 1];
-#pragma unroll
-  for (int i = 0; i <= L; i++) acc[i] = 0;
-  int64_t S = 0;  // sum of coefficients (bias correction)
-
-  // +-1 entries
   const uint4* pp = a.pm_idx + si.pm_off + rw;
 #pragma unroll 1
   for (uint32_t k = 0; k < my_pm; k++) {
@@ -379,46 +360,65 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
       }
     }
   }
-  if (!FIRST) {
-    uint32_t pin[SW];
-    load_slot<SW>(a.part_in + ((size_t)slot * G + chain) * SW, pin, pol);
-#pragma unroll
-    for (int i = 0; i < L; i++) acc[i] += pin[i];
-  }
-  const int32_t row = LAST ? a.slot_row[slot] : 0;
-  if (LAST && a.has_full) {
-    // full-class coefficients (f*u mod ell by Montgomery: f stored as f R)
+}
+
+// full-class coefficients and dense columns of one row (last pass only):
+// f*u mod ell by Montgomery, f stored as f R
+template <int L, int G>
+__device__ __forceinline__ void row_full(const SpmvArgs& a, const ModParams& mp, int64_t slot, int32_t row,
+                                         const uint32_t* xc, int64_t (&acc)[L + 1]) {
+  constexpr int SW = stride_words(L);
 #pragma unroll 1
-    for (uint32_t p = a.full_ptr[slot]; p < a.full_ptr[slot + 1]; p++) {
-      uint32_t u[SW], f[L], r[L];
-      gather<SW>(xc + (size_t)a.full_col[p] * (G * SW), u);
+  for (uint32_t p = a.full_ptr[slot]; p < a.full_ptr[slot + 1]; p++) {
+    uint32_t u[SW], f[L], r[L];
+    gather<SW>(xc + (size_t)a.full_col[p] * (G * SW), u);
 #pragma unroll
-      for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; f[i] = a.full_val[(size_t)p * SW + i]; }
+    for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; f[i] = a.full_val[(size_t)p * SW + i]; }
+    montmul<L>(f, u, mp, r);
+#pragma unroll
+    for (int i = 0; i < L; i++) acc[i] += r[i];
+  }
+  if (row >= 0) {
+#pragma unroll 1
+    for (int g = 0; g < a.n_dense; g++) {
+      uint32_t u[SW], f[L], r[L];
+      gather<SW>(xc + (size_t)(a.dense_col0 + g) * (G * SW), u);
+#pragma unroll
+      for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; }
+      // dense values: [g][row], rows padded to nslots
+      const uint32_t* dv = a.dense_val + ((size_t)g * (size_t)a.nslots + (size_t)row) * SW;
+#pragma unroll
+      for (int i = 0; i < L; i++) f[i] = dv[i];
       montmul<L>(f, u, mp, r);
 #pragma unroll
       for (int i = 0; i < L; i++) acc[i] += r[i];
     }
-    if (row >= 0) {
-#pragma unroll 1
-      for (int g = 0; g < a.n_dense; g++) {
-        uint32_t u[SW], f[L], r[L];
-        gather<SW>(xc + (size_t)(a.dense_col0 + g) * (G * SW), u);
-#pragma unroll
-        for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; }
-        // dense values: [g][row], rows padded to nslots
-        const uint32_t* dv = a.dense_val + ((size_t)g * (size_t)a.nslots + (size_t)row) * SW;
-#pragma unroll
-        for (int i = 0; i < L; i++) f[i] = dv[i];
-        montmul<L>(f, u, mp, r);
-#pragma unroll
-        for (int i = 0; i < L; i++) acc[i] += r[i];
-      }
-    }
   }
-  uint32_t Rr[L];
-  finalize<L>(acc, S, mp, Rr);
+}
+
+// a_i = X^T v_i of the iterate this product consumes (solver.py:210): the
+// first threads of block 0 copy the m unit-X rows of the INPUT iterate
+template <int L, int G>
+__device__ __forceinline__ void unit_projection(const SpmvArgs& a) {
+  constexpr int SW = stride_words(L);
+  if (blockIdx.x == 0 && threadIdx.x < a.proj_m * G) {
+    const int t = threadIdx.x / G, c = threadIdx.x % G;
+    const uint32_t* src = a.x + ((size_t)a.proj_rows[t] * G + c) * SW;
+    uint32_t* dst = a.terms_out + ((size_t)t * G + c) * SW;
+#pragma unroll
+    for (int i = 0; i < SW; i++) dst[i] = i < L ? (src[i] ^ 0x80000000u) : 0u;
+  }
+}
+
+// store a finished canonical row value: biased into y (last pass) or
+// canonical into the slot-indexed partial (more passes follow)
+template <int L, int G, bool LAST>
+__device__ __forceinline__ void store_row(const SpmvArgs& a, int64_t slot, int chain, const uint32_t (&Rr)[L],
+                                          uint64_t pol) {
+  constexpr int SW = stride_words(L);
   uint32_t o[SW];
   if (LAST) {
+    const int32_t row = a.slot_row[slot];
     if (row < 0) return;
 #pragma unroll
     for (int i = 0; i < SW; i++) o[i] = i < L ? (Rr[i] ^ 0x80000000u) : 0u;
@@ -431,6 +431,192 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
     uint32_t* dst = a.part_out + ((size_t)slot * G + chain) * SW;
     if (a.policy & 4) store_slot_hint<SW>(dst, o, pol);
     else store_slot<SW>(dst, o);
+  }
+}
+
+template <int L, int G, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const SpmvArgs a, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  constexpr int R = 32 / G;  // rows per warp = slice height
+  const int lane = threadIdx.x & 31;
+  const int chain = lane & (G - 1);
+  const int rw = lane / G;
+  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t slot = slice * R + rw;
+
+  if (FIRST) unit_projection<L, G>(a);
+  if (slice >= a.nslices) return;
+
+  const uint64_t pol = policy_evict_first();
+  const uint64_t gpol = (a.policy & 1) ? policy_evict_last() : createpolicy_normal();
+  const SliceInfo si = a.slices[slice];
+  // per-row group counts: lanes stop at their own row length, so padded
+  // SELL positions are never loaded (no index or gather traffic)
+  const uint32_t kk = a.lane_k4[slot];
+  const uint32_t* xc = a.x + (size_t)chain * SW;  // this lane's chain in every record
+  int64_t acc[L + 1];
+#pragma unroll
+  for (int i = 0; i <= L; i++) acc[i] = 0;
+  int64_t S = 0;  // sum of coefficients (bias correction)
+  row_entries<L, G>(a, si, kk, rw, xc, pol, gpol, acc, S);
+  if (!FIRST) {
+    uint32_t pin[SW];
+    load_slot<SW>(a.part_in + ((size_t)slot * G + chain) * SW, pin, pol);
+#pragma unroll
+    for (int i = 0; i < L; i++) acc[i] += pin[i];
+  }
+  if (LAST && a.has_full) row_full<L, G>(a, mp, slot, a.slot_row[slot], xc, acc);
+  uint32_t Rr[L];
+  finalize<L>(acc, S, mp, Rr);
+  store_row<L, G, LAST>(a, slot, chain, Rr, pol);
+}
+
+// ------------------------------------------------- die-split SpMV pass
+//
+// B200 is two dies, and each die's L2 keeps its own copy of every line its
+// SMs read: a randomly gathered working set thrashes beyond ~one die's L2
+// (~63 MB) when every SM gathers every column, but stays resident up to
+// ~128 MB when the SMs of die d only gather the columns of half d
+// (tools/microbench/mb3.cu, profiles/microbench3_r01.txt).  The columns are
+// therefore dealt to two halves (interleaved chunks, sized to the dies' SM
+// counts) and every row gets one partial result per half:
+//  * a persistent grid; each CTA finds its die from %smid (die map probed at
+//    context creation) and warps take slices from that die's work queue,
+//    then steal from the other queue once theirs is empty (correctness
+//    never depends on where CTAs land);
+//  * the two partial results of a row meet through an exchange buffer: each
+//    half stores its canonical value, fences, and bumps the slice's arrival
+//    counter; the second to arrive (odd count) adds the other's value mod
+//    ell and writes the row.  Counters grow by 2 per pass, so parity marks
+//    the order without ever being reset;
+//  * half 0 also carries the previous pass's partial and, on the last pass,
+//    the full-class entries and dense columns;
+//  * the last warp to leave resets the work queues for the next launch.
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+
+// r = a + b mod ell for canonical a, b
+template <int L>
+__device__ __forceinline__ void add_canonical(const uint32_t (&a_)[L], const uint32_t (&b)[L],
+                                              const ModParams& mp, uint32_t (&r)[L]) {
+  uint32_t s[L];
+  uint64_t c = 0;
+#pragma unroll
+  for (int j = 0; j < L; j++) {
+    c = (uint64_t)a_[j] + b[j] + (c >> 32);
+    s[j] = (uint32_t)c;
+  }
+  const int64_t top = (int64_t)(c >> 32);
+  int64_t br = 0;
+  uint32_t d[L];
+#pragma unroll
+  for (int j = 0; j < L; j++) {
+    const int64_t v = (int64_t)s[j] - mp.ell[j] + br;
+    d[j] = (uint32_t)v;
+    br = v >> 32;
+  }
+  const bool ge = top + br >= 0;  // s >= ell
+#pragma unroll
+  for (int j = 0; j < L; j++) r[j] = ge ? d[j] : s[j];
+}
+
+constexpr int SPLIT_GRAB = 2;  // slices a warp takes per queue ticket
+
+template <int L, int G, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_split(const SpmvArgs a, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  constexpr int R = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int chain = lane & (G - 1);
+  const int rw = lane / G;
+  if (FIRST) unit_projection<L, G>(a);
+
+  const uint64_t pol = policy_evict_first();
+  const uint64_t gpol = (a.policy & 1) ? policy_evict_last() : createpolicy_normal();
+  const uint32_t* xc = a.x + (size_t)chain * SW;
+  const int home = a.die_map[sm_id() & 255];
+  const uint32_t nsl = (uint32_t)a.nslices;
+  const size_t xstride = (size_t)a.nslots * G * SW;
+#pragma unroll 1
+  for (int pass_h = 0; pass_h < 2; pass_h++) {
+    const int h = home ^ pass_h;  // own die's queue first, then help the other
+    const SliceInfo* slices = a.slices + (size_t)h * a.nslices;
+    const uint32_t* lk = a.lane_k4 + (size_t)h * a.nslots;
+    uint32_t* xmine = a.xch + (size_t)h * xstride;
+    const uint32_t* xother = a.xch + (size_t)(h ^ 1) * xstride;
+#pragma unroll 1
+    while (true) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(a.queue + h, SPLIT_GRAB);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= nsl) break;
+#pragma unroll 1
+      for (uint32_t slice = base; slice < min(base + SPLIT_GRAB, nsl); slice++) {
+        const int64_t slot = (int64_t)slice * R + rw;
+        const SliceInfo si = slices[slice];
+        int64_t acc[L + 1];
+#pragma unroll
+        for (int i = 0; i <= L; i++) acc[i] = 0;
+        int64_t S = 0;
+        row_entries<L, G>(a, si, lk[slot], rw, xc, pol, gpol, acc, S);
+        if (h == 0) {
+          if (!FIRST) {
+            uint32_t pin[SW];
+            load_slot<SW>(a.part_in + ((size_t)slot * G + chain) * SW, pin, pol);
+#pragma unroll
+            for (int i = 0; i < L; i++) acc[i] += pin[i];
+          }
+          if (LAST && a.has_full) row_full<L, G>(a, mp, slot, a.slot_row[slot], xc, acc);
+        }
+        uint32_t Rr[L];
+        finalize<L>(acc, S, mp, Rr);
+        // publish this half's value, then count the arrival
+        {
+          uint32_t o[SW];
+#pragma unroll
+          for (int i = 0; i < SW; i++) o[i] = i < L ? Rr[i] : 0u;
+          store_slot<SW>(xmine + ((size_t)slot * G + chain) * SW, o);
+        }
+        // (the grid-barrier pattern: warp barrier, then one fenced atomic)
+        __syncwarp();
+        uint32_t old = 0;
+        if (lane == 0) {
+          __threadfence();
+          old = atomicAdd(a.cnt + slice, 1u);
+          if (old & 1u) __threadfence();
+        }
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old & 1u) {  // second to arrive: combine and write the row
+          uint32_t pv[SW], P[L];
+          const uint32_t* src = xother + ((size_t)slot * G + chain) * SW;
+#pragma unroll
+          for (int q = 0; q < SW / 8; q++)
+            asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(pv[8 * q + 0]), "=r"(pv[8 * q + 1]), "=r"(pv[8 * q + 2]), "=r"(pv[8 * q + 3]),
+                           "=r"(pv[8 * q + 4]), "=r"(pv[8 * q + 5]), "=r"(pv[8 * q + 6]), "=r"(pv[8 * q + 7])
+                         : "l"(src + 8 * q)
+                         : "memory");
+#pragma unroll
+          for (int i = 0; i < L; i++) P[i] = pv[i];
+          uint32_t Sum[L];
+          add_canonical<L>(Rr, P, mp, Sum);
+          store_row<L, G, LAST>(a, slot, chain, Sum, pol);
+        }
+      }
+    }
+  }
+  // the last warp out resets the queues for the next launch
+  if (lane == 0) {
+    const uint32_t total = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(a.queue + 2, 1u) == total - 1) {
+      a.queue[0] = 0;
+      a.queue[1] = 0;
+      a.queue[2] = 0;
+      __threadfence();
+    }
   }
 }
 

@@ -17,6 +17,11 @@ struct LOps {
   // returns false if G is not supported for this L
   bool (*pass)(int G, int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
                const ModParams& mp);
+  // die-split pass on a persistent grid of `grid` CTAs (false: G unsupported)
+  bool (*split)(int G, int first, int last, unsigned grid, cudaStream_t s, const SpmvArgs& a,
+                const ModParams& mp);
+  // resident CTAs per SM of the die-split kernel for G chains (0: unsupported)
+  int (*split_occupancy)(int G);
   void (*limbs_to_slots)(const uint32_t*, int64_t, uint32_t*, uint32_t, int64_t, int, cudaStream_t);
   void (*slots_to_limbs)(const uint32_t*, int64_t, uint32_t*, uint32_t, int64_t, int, cudaStream_t);
   void (*to_mont)(uint32_t*, int64_t, const ModParams&, cudaStream_t);
@@ -37,6 +42,23 @@ void launch_pass(int first, int last, unsigned grid, cudaStream_t s, const SpmvA
   else if (first) spmv_pass<L, G, true, false><<<grid, 256, 0, s>>>(a, mp);
   else if (last) spmv_pass<L, G, false, true><<<grid, 256, 0, s>>>(a, mp);
   else spmv_pass<L, G, false, false><<<grid, 256, 0, s>>>(a, mp);
+}
+
+template <int L, int G>
+void launch_split(int first, int last, unsigned grid, cudaStream_t s, const SpmvArgs& a,
+                  const ModParams& mp) {
+  if (first && last) spmv_split<L, G, true, true><<<grid, 256, 0, s>>>(a, mp);
+  else if (first) spmv_split<L, G, true, false><<<grid, 256, 0, s>>>(a, mp);
+  else if (last) spmv_split<L, G, false, true><<<grid, 256, 0, s>>>(a, mp);
+  else spmv_split<L, G, false, false><<<grid, 256, 0, s>>>(a, mp);
+}
+
+template <int L, int G>
+int split_occ() {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_split<L, G, false, false>, 256, 0) != cudaSuccess)
+    return 0;
+  return n;
 }
 
 template <int L>
@@ -61,6 +83,34 @@ struct Ops {
       }
     }
     return false;
+  }
+  static bool split(int G, int first, int last, unsigned grid, cudaStream_t s, const SpmvArgs& a,
+                    const ModParams& mp) {
+    if (G == 1) {
+      launch_split<L, 1>(first, last, grid, s, a, mp);
+      return true;
+    }
+    if constexpr (max_chains(L) >= 2) {
+      if (G == 2) {
+        launch_split<L, 2>(first, last, grid, s, a, mp);
+        return true;
+      }
+    }
+    if constexpr (max_chains(L) >= 4) {
+      if (G == 4) {
+        launch_split<L, 4>(first, last, grid, s, a, mp);
+        return true;
+      }
+    }
+    return false;
+  }
+  static int split_occupancy(int G) {
+    if (G == 1) return split_occ<L, 1>();
+    if constexpr (max_chains(L) >= 2)
+      if (G == 2) return split_occ<L, 2>();
+    if constexpr (max_chains(L) >= 4)
+      if (G == 4) return split_occ<L, 4>();
+    return 0;
   }
   static void l2s(const uint32_t* l, int64_t n, uint32_t* o, uint32_t b, int64_t rows, int G,
                   cudaStream_t s) {
@@ -89,7 +139,7 @@ struct Ops {
   static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
     if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);
   }
-  static LOps make() { return LOps{pass, l2s, s2l, mont, zero, dproj, addm, rrows, lcomb, nz}; }
+  static LOps make() { return LOps{pass, split, split_occupancy, l2s, s2l, mont, zero, dproj, addm, rrows, lcomb, nz}; }
 };
 
 template <int L, int LMIN>

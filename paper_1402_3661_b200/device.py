@@ -188,7 +188,7 @@ class DeviceMatrix:
 
     INFO_KEYS = ("nrows", "total_cols", "nnz", "n_pm", "n_small", "n_full", "stripes",
                  "nslices", "device_bytes", "pad_entries", "L", "stride_words", "max_degree",
-                 "stripe_cols", "chains")
+                 "stripe_cols", "chains", "halves")
 
     def __init__(self, A, device=None, stripe_cols=0, field=None, chains=1):
         self.mod = as_modulus(A.mod)

@@ -22,11 +22,20 @@ def main():
     ap.add_argument("--stripes", default="0")
     ap.add_argument("--apw", default="0", help="comma list of SLD_APW_RATIO values; 0 = off")
     ap.add_argument("--chains", default="1", help="comma list of chains per matrix pass")
+    ap.add_argument("--split", default="", help="comma list of SLD_SPLIT values (die split off/on)")
+    ap.add_argument("--frac", default="", help="comma list of SLD_SPLIT_FRAC values")
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
     y = _random_residue_limbs(np.random.default_rng(5), A.total_cols, mod)
-    for G in [int(x) for x in a.chains.split(",")]:
+    splits = [(sp, fr) for sp in (a.split.split(",") if a.split else [""])
+              for fr in (a.frac.split(",") if a.frac else [""])]
+    for G, (sp, fr) in [(int(x), s) for x in a.chains.split(",") for s in splits]:
+      for k, val in (("SLD_SPLIT", sp), ("SLD_SPLIT_FRAC", fr)):
+          if val:
+              os.environ[k] = val
+          else:
+              os.environ.pop(k, None)
       for sc in [int(x) for x in a.stripes.split(",")]:
         for pol, apw in [(int(x), float(y)) for x in a.policies.split(",") for y in a.apw.split(",")]:
             os.environ["SLD_POLICY"] = str(pol)
@@ -45,7 +54,9 @@ def main():
             import subprocess
             clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.mem,power.draw,temperature.gpu",
                                   "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
-            print(f"{a.config} G={G} stripes={dm.info()['stripes']} policy={pol} apw={apw}: "
+            inf = dm.info()
+            print(f"{a.config} G={G} stripes={inf['stripes']} halves={inf['halves']} split_frac={fr or '-'} "
+                  f"policy={pol} apw={apw}: "
                   f"{per:.4f} ms/pass = {per / G:.4f} ms per chain-product  [{clk}]",
                   flush=True)
             v.close()
