@@ -161,6 +161,7 @@ struct sld_mat {
   int64_t max_deg = 0;
   size_t dev_bytes = 0;
   int policy = 7;  // L2 policy bits (SpmvArgs::policy), measured best; env SLD_POLICY overrides
+  int pf = 2;      // index prefetch distance in groups, measured; env SLD_PF overrides
   int apw = 0;       // persisting L2 access-policy window over the gathered stripe (env SLD_APW)
   float apw_ratio = 1.0f;
   // device
@@ -175,11 +176,13 @@ struct sld_mat {
   uint32_t* full_val = nullptr;
   uint32_t* dense_val = nullptr;
   uint32_t* part = nullptr;  // slot-indexed partials (npass > 1)
+  // limb-sliced passes (one chain, L > 8): T lanes per row, 32 / T rows per slice
+  int sliced = 0;
   // die split (halves == 2): each pass's columns are dealt to the two dies
   int halves = 1;
   int64_t half_chunk = 0;      // columns per interleaved chunk
   unsigned split_grid = 0;     // persistent CTAs of the split kernel
-  uint32_t* xch = nullptr;     // [2][nslots * G * SW]
+  uint32_t* xch = nullptr;     // [nslots * G * SW]
   uint32_t* cnt = nullptr;     // [nslices] arrival counters
   uint32_t* queue = nullptr;   // [4] work queues + exit counter
   // host-planes convenience staging
@@ -236,17 +239,19 @@ __global__ void die_discard(uint32_t* buf) {
   if (i < DIE_PROBES) asm volatile("discard.global.L2 [%0], 128;" ::"l"(buf + (size_t)i * DIE_STRIDE) : "memory");
 }
 __global__ void die_time(const uint32_t* buf, int target, uint32_t* lat, int* hit) {
+  __shared__ uint32_t sink[2];
   if (sm_id() != (uint32_t)target || threadIdx.x != 0) return;
   if (atomicExch(hit, 1) != 0) return;
-  uint32_t dep = 0;
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sink);
   for (int i = 0; i < DIE_PROBES; i++) {
-    const uint32_t* p = buf + (size_t)i * DIE_STRIDE + dep;
     uint64_t t0, t1;
     uint32_t v;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0) : "r"(dep) : "memory");
-    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    dep = v >> 31 & 0u;  // 0, but the clock read below waits for the load
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1) : "r"(v) : "memory");
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0)::"memory");
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(buf + (size_t)i * DIE_STRIDE) : "memory");
+    // the volatile shared store consumes the load, and the clock read is
+    // not moved above a memory operation
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(sa), "r"(v) : "memory");
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1)::"memory");
     lat[i] = (uint32_t)(t1 - t0);
   }
 }
@@ -264,54 +269,83 @@ DieMap g_die[64];
 int probe_dies(int dev, DieMap& d, int sms) {
   uint32_t *buf = nullptr, *lat = nullptr;
   int *hit = nullptr, *nsm = nullptr;
-  const int T = 256;
+  const int T = 256, REPS = 3;  // min over repetitions drops DRAM latency spikes
   CU(cudaMalloc(&buf, (size_t)DIE_PROBES * DIE_STRIDE * 4 + 256));
-  CU(cudaMalloc(&lat, (size_t)T * DIE_PROBES * 4));
-  CU(cudaMalloc(&hit, T * 4));
+  CU(cudaMalloc(&lat, (size_t)REPS * T * DIE_PROBES * 4));
+  CU(cudaMalloc(&hit, REPS * T * 4));
   CU(cudaMalloc(&nsm, 4));
   CU(cudaMemset(buf, 0, (size_t)DIE_PROBES * DIE_STRIDE * 4 + 256));
-  CU(cudaMemset(hit, 0, T * 4));
+  CU(cudaMemset(hit, 0, REPS * T * 4));
   die_nsmid<<<1, 1>>>(nsm);
   int nsmid = 0;
   CU(cudaMemcpy(&nsmid, nsm, 4, cudaMemcpyDeviceToHost));
   nsmid = std::min(std::max(nsmid, sms), T);
-  for (int t = 0; t < nsmid; t++) {
-    die_discard<<<1, DIE_PROBES>>>(buf);
-    die_time<<<sms * 4, 32>>>(buf, t, lat + (size_t)t * DIE_PROBES, hit + t);
-  }
-  std::vector<uint32_t> L((size_t)T * DIE_PROBES);
-  std::vector<int> H(T);
-  CU(cudaMemcpy(L.data(), lat, L.size() * 4, cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(H.data(), hit, T * 4, cudaMemcpyDeviceToHost));
+  for (int r = 0; r < REPS; r++)
+    for (int t = 0; t < nsmid; t++) {
+      die_discard<<<1, DIE_PROBES>>>(buf);
+      die_time<<<sms * 4, 32>>>(buf, t, lat + ((size_t)r * T + t) * DIE_PROBES, hit + r * T + t);
+    }
+  std::vector<uint32_t> LR((size_t)REPS * T * DIE_PROBES), L((size_t)T * DIE_PROBES, ~0u);
+  std::vector<int> HR(REPS * T), H(T, 1);
+  CU(cudaMemcpy(LR.data(), lat, LR.size() * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(HR.data(), hit, HR.size() * 4, cudaMemcpyDeviceToHost));
+  for (int r = 0; r < REPS; r++)
+    for (int t = 0; t < T; t++) {
+      H[t] &= HR[r * T + t];
+      for (int i = 0; i < DIE_PROBES; i++)
+        L[(size_t)t * DIE_PROBES + i] = std::min(L[(size_t)t * DIE_PROBES + i], LR[((size_t)r * T + t) * DIE_PROBES + i]);
+    }
   cudaFree(buf);
   cudaFree(lat);
   cudaFree(hit);
   cudaFree(nsm);
-  // near/far pattern of each SM against its own midpoint
-  std::vector<uint8_t> ref;
-  d.ok = true;
-  for (int t = 0; t < nsmid && d.ok; t++) {
+  if (getenv("SLD_DIE_DEBUG")) {
+    for (int t = 0; t < nsmid; t++) {
+      if (!H[t]) continue;
+      fprintf(stderr, "die probe sm %3d:", t);
+      for (int i = 0; i < 24; i++) fprintf(stderr, " %u", L[(size_t)t * DIE_PROBES + i]);
+      fprintf(stderr, "\n");
+    }
+  }
+  // Measured on B200 (profiles/die_probe_r01.txt): after the discard, SMs of
+  // one die see ~600/~980 cycles (near/far HBM), SMs of the other ~300/~600
+  // (the lines are still served from the first die's L2), with the same
+  // per-line pattern.  Either way the per-SM mean latency falls into two
+  // clusters, one per die: split at the widest gap of the sorted means.
+  std::vector<std::pair<double, int>> mean;
+  for (int t = 0; t < nsmid; t++) {
     if (!H[t]) continue;
-    const uint32_t* l = &L[(size_t)t * DIE_PROBES];
-    const uint32_t lo = *std::min_element(l, l + DIE_PROBES), hi = *std::max_element(l, l + DIE_PROBES);
-    if (hi - lo < 150) {
-      d.ok = false;
-      d.why = "no near/far latency split on sm " + std::to_string(t);
-      break;
+    double m = 0;
+    for (int i = 0; i < DIE_PROBES; i++) m += L[(size_t)t * DIE_PROBES + i];
+    mean.push_back({m / DIE_PROBES, t});
+  }
+  std::sort(mean.begin(), mean.end());
+  size_t cut = 0;
+  double gap = 0;
+  for (size_t k = 1; k < mean.size(); k++)
+    if (mean[k].first - mean[k - 1].first > gap) {
+      gap = mean[k].first - mean[k - 1].first;
+      cut = k;
     }
-    std::vector<uint8_t> near(DIE_PROBES);
-    for (int i = 0; i < DIE_PROBES; i++) near[i] = l[i] * 2 < lo + hi;
-    if (ref.empty()) ref = near;
-    int agree = 0;
-    for (int i = 0; i < DIE_PROBES; i++) agree += near[i] == ref[i];
-    if (agree >= DIE_PROBES * 9 / 10) d.map[t] = 0;
-    else if (agree <= DIE_PROBES / 10) d.map[t] = 1;
-    else {
-      d.ok = false;
-      d.why = "ambiguous near/far pattern on sm " + std::to_string(t);
-      break;
+  d.ok = true;
+  const double spread0 = mean.empty() ? 0 : mean[cut ? cut - 1 : 0].first - mean[0].first;
+  const double spread1 = mean.empty() ? 0 : mean.back().first - mean[cut].first;
+  if (mean.size() < 2 || gap < 100 || gap < 2 * std::max(spread0, spread1) || cut < 8 || mean.size() - cut < 8) {
+    d.ok = false;
+    d.why = "no two-cluster latency split (gap " + std::to_string((int)gap) + " cycles)";
+  } else {
+    // label the die of the lowest smid 0
+    const int first = std::min_element(mean.begin(), mean.end(),
+                                       [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
+                                         return a.second < b.second;
+                                       })->second;
+    bool first_low = false;
+    for (size_t k = 0; k < cut; k++) first_low |= mean[k].second == first;
+    for (size_t k = 0; k < mean.size(); k++) {
+      const int die = (k < cut) == first_low ? 0 : 1;
+      d.map[mean[k].second] = (uint8_t)die;
+      d.n[die]++;
     }
-    d.n[d.map[t]]++;
   }
   if (d.ok && (d.n[0] == 0 || d.n[1] == 0)) {
     d.ok = false;
@@ -851,10 +885,12 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   {
     // measured (tools/microbench/mb3.cu): with every SM gathering every
     // column the L2 holds ~one die's worth (~63 MB); dealing the columns to
-    // the dies keeps ~128 MB resident.  Split once the vector outgrows ~0.4 L2.
-    int want = vec_bytes > 0.4 * l2 ? 1 : 0;
+    // the dies keeps ~128 MB resident.  In the SpMV the per-slice meeting of
+    // the halves costs more than the fewer stripes save (cfg3: 1.63 vs
+    // 1.36 ms per chain-product), so the split is opt-in.
+    int want = 0;
     if (const char* e = getenv("SLD_SPLIT")) want = atoi(e);
-    if (want && c->die_n[0] > 0 && c->die_n[1] > 0 && nrows > 0 &&
+    if (want && !M->sliced && c->die_n[0] > 0 && c->die_n[1] > 0 && nrows > 0 &&
         ops(L).split_occupancy(M->chains) > 0)
       H = 2;
   }
@@ -957,7 +993,8 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     if (tot_pm[x] != tot_pm[y]) return tot_pm[x] > tot_pm[y];
     return tot_s[x] > tot_s[y];
   });
-  const int RH = 32 / M->chains;  // rows per slice (one warp: RH rows x G chains)
+  // rows per slice: one warp holds RH rows x G chains, or RH rows x T limb slices
+  const int RH = M->sliced ? 32 / (SW / 8) : 32 / M->chains;
   const int64_t nslices = (nrows + RH - 1) / RH;
   M->nslices = nslices;
   const int64_t nslots = nslices * RH;
@@ -1126,7 +1163,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     acct += (size_t)nslots * M->chains * SW * 4;
   }
   if (H == 2) {
-    const size_t xb = (size_t)2 * nslots * M->chains * SW * 4;
+    const size_t xb = (size_t)nslots * M->chains * SW * 4;
     CU(cudaMalloc(&M->xch, xb));
     CU(cudaMalloc(&M->cnt, std::max<size_t>((size_t)nslices * 4, 16)));
     CU(cudaMemset(M->cnt, 0, std::max<size_t>((size_t)nslices * 4, 16)));
@@ -1171,6 +1208,13 @@ extern "C" int sld_mat_create_chains(sld_ctx* ctx, int chains, int64_t nrows, in
   M->total_cols = ncols + n_dense;
   M->nnz = nnz;
   if (const char* pe = getenv("SLD_POLICY")) M->policy = atoi(pe);
+  if (const char* pe = getenv("SLD_PF")) M->pf = std::max(0, atoi(pe));
+  {
+    // measured: one request per gathered residue instead of SW/8 (cfg5 ...)
+    int wide = 1;
+    if (const char* pe = getenv("SLD_WIDE")) wide = atoi(pe);
+    M->sliced = (wide && chains == 1 && ctx->SW >= 16) ? 1 : 0;
+  }
   if (const char* pe = getenv("SLD_APW")) M->apw = atoi(pe);
   if (const char* pe = getenv("SLD_APW_RATIO")) M->apw_ratio = (float)atof(pe);
   int r = mat_build(M, row_ptr, col_idx, tags, small_vals, n_full, full_pos, full_limbs, dense_limbs,
@@ -1221,6 +1265,7 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
   a.nslots = M->nslots;
   a.has_full = (M->full_ptr && M->n_full) ? 1 : 0;
   a.policy = M->policy;
+  a.pf = (uint32_t)M->pf;
   const LOps& o = ops(c->L);
   if (M->nslices == 0) {
     // no rows: still record the projection
@@ -1247,6 +1292,10 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
   for (int p = 0; p < M->npass; p++) {
     a.slices = M->slices + (size_t)p * M->nslices;
     a.lane_k4 = M->lane_k4 + (size_t)p * M->nslots;
+    if (M->sliced) {
+      o.wide(p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
+      continue;
+    }
     if (M->apw && c->apw_max) {
       // persisting L2 window over the stripe this pass gathers from
       const int64_t lo = (int64_t)p * M->stripe_cols;

@@ -66,9 +66,10 @@ struct SpmvArgs {
   // die-split passes (spmv_split): slices / lane_k4 hold both halves, half h
   // at offset h * nslices / h * nslots
   const uint8_t* die_map;  // %smid -> die (0/1)
-  uint32_t* xch;           // [2][nslots * G * SW] the halves' row values
+  uint32_t* xch;           // [nslots * G * SW] the first half's row values
   uint32_t* cnt;           // [nslices] arrival counters (parity = order)
   uint32_t* queue;         // [3] work queue per die + exit counter
+  uint32_t pf;             // index groups prefetched into L2 ahead of use
 };
 
 // ---------------------------------------------------------------- loads
@@ -303,6 +304,16 @@ __host__ __device__ constexpr int spmv_batch() { return L <= 8 ? 4 : (L <= 16 ? 
 // (~1 sector-request per SM per clock, profiles/microbench2_r01.txt), so a
 // 2-sector record moves ~1.7x the useful bytes per second of a 1-sector one.
 
+// Index-stream prefetch: each lane asks L2 for its index group PF groups
+// ahead of the one it consumes, so the DRAM latency of the read-once index
+// stream overlaps the gathers of the groups before it.  (A shared-memory
+// cp.async ring was measured slower: its 33 KB per CTA come out of the L1
+// that stages the outstanding gathers.)
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p));
+}
+
 // the +-1 and small entries of one row in one part (column stripe [x half])
 template <int L, int G>
 __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& si, uint32_t kk, int rw,
@@ -312,9 +323,13 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
   constexpr int NB = spmv_batch<L>();
   constexpr int R = 32 / G;
   const uint32_t my_pm = kk & 0xFFFFu, my_s = kk >> 16;
+  const uint32_t PF = a.pf;  // prefetch distance in groups (0: off)
   const uint4* pp = a.pm_idx + si.pm_off + rw;
 #pragma unroll 1
+  for (uint32_t k = 0; k < PF && k < my_pm; k++) prefetch_l2(pp + (size_t)k * R);
+#pragma unroll 1
   for (uint32_t k = 0; k < my_pm; k++) {
+    if (PF && k + PF < my_pm) prefetch_l2(pp + (size_t)(k + PF) * R);
     const uint4 w = ld_stream(pp + (size_t)k * R, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -337,7 +352,16 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
   const uint4* sp = a.s_idx + si.s_off + rw;
   const int4* cp = a.s_coef + si.s_off + rw;
 #pragma unroll 1
+  for (uint32_t k = 0; k < PF && k < my_s; k++) {
+    prefetch_l2(sp + (size_t)k * R);
+    prefetch_l2(cp + (size_t)k * R);
+  }
+#pragma unroll 1
   for (uint32_t k = 0; k < my_s; k++) {
+    if (PF && k + PF < my_s) {
+      prefetch_l2(sp + (size_t)(k + PF) * R);
+      prefetch_l2(cp + (size_t)(k + PF) * R);
+    }
     const uint4 w = ld_stream(sp + (size_t)k * R, pol);
     const int4 cf = ld_stream(cp + (size_t)k * R, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
@@ -471,6 +495,158 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
   store_row<L, G, LAST>(a, slot, chain, Rr, pol);
 }
 
+// ------------------------------------------------ limb-sliced SpMV pass
+//
+// Wide moduli (L > 8: residues of T = SW/8 >= 2 sectors).  Random gathers
+// are request-bound (~1 request per SM per clock), and a residue loaded by
+// one lane costs T requests.  Here the T lanes of a row each own one 32-byte
+// slice (8 limbs) of every residue, so one instruction of the T lanes loads a
+// whole residue as ONE request, and the per-lane accumulator is 8 limbs wide
+// whatever L is.  Per row, the lanes then normalise their slices, pass the
+// carries up the row with shuffles, hand the words to the row's first lane,
+// and that lane runs the same tail as spmv_pass (partial, full-class
+// entries, Barrett finalize, store).  Rows per warp: RH = 32 / T.
+template <int L>
+__host__ __device__ constexpr int wide_T() { return stride_words(L) / 8; }
+
+template <int L, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(256, 3) spmv_wide(const SpmvArgs a, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  constexpr int T = wide_T<L>();
+  constexpr int RH = 32 / T;
+  constexpr int NB = 4;
+  const int lane = threadIdx.x & 31;
+  const int rw = lane / T, sl = lane % T;  // row in the slice, limb slice of the residue
+  const bool active = rw < RH;
+  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t slot = slice * RH + (active ? rw : 0);
+
+  if (FIRST) unit_projection<L, 1>(a);
+  if (slice >= a.nslices) return;
+
+  const uint64_t pol = policy_evict_first();
+  const uint64_t gpol = (a.policy & 1) ? policy_evict_last() : createpolicy_normal();
+  const SliceInfo si = a.slices[slice];
+  const uint32_t kk = active ? a.lane_k4[slot] : 0u;
+  const uint32_t my_pm = kk & 0xFFFFu, my_s = kk >> 16;
+  const uint32_t* xs = a.x + sl * 8;  // this lane's slice of every record
+  int64_t acc[9];  // words 8 sl .. 8 sl + 7, and the small products' spill into the next slice
+#pragma unroll
+  for (int i = 0; i < 9; i++) acc[i] = 0;
+  int64_t S = 0;
+  const uint32_t PF = a.pf;
+  const uint4* pp = a.pm_idx + si.pm_off + rw;
+#pragma unroll 1
+  for (uint32_t k = 0; k < PF && k < my_pm; k++) prefetch_l2(pp + (size_t)k * RH);
+#pragma unroll 1
+  for (uint32_t k = 0; k < my_pm; k++) {
+    if (PF && k + PF < my_pm) prefetch_l2(pp + (size_t)(k + PF) * RH);
+    const uint4 w = ld_stream(pp + (size_t)k * RH, pol);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint32_t u[NB][8];
+#pragma unroll
+    for (int e = 0; e < NB; e++) gather_hint<8>(xs + (size_t)(ws[e] & 0x7FFFFFFFu) * SW, u[e], gpol);
+#pragma unroll
+    for (int e = 0; e < NB; e++) {
+      const int32_t c = 1 - (int32_t)((ws[e] >> 30) & 2u);
+      S += c;
+#pragma unroll
+      for (int i = 0; i < 8; i++) acc[i] += (int64_t)c * (int64_t)(int32_t)u[e][i];
+    }
+  }
+  const uint4* sp = a.s_idx + si.s_off + rw;
+  const int4* cp = a.s_coef + si.s_off + rw;
+#pragma unroll 1
+  for (uint32_t k = 0; k < PF && k < my_s; k++) {
+    prefetch_l2(sp + (size_t)k * RH);
+    prefetch_l2(cp + (size_t)k * RH);
+  }
+#pragma unroll 1
+  for (uint32_t k = 0; k < my_s; k++) {
+    if (PF && k + PF < my_s) {
+      prefetch_l2(sp + (size_t)(k + PF) * RH);
+      prefetch_l2(cp + (size_t)(k + PF) * RH);
+    }
+    const uint4 w = ld_stream(sp + (size_t)k * RH, pol);
+    const int4 cf = ld_stream(cp + (size_t)k * RH, pol);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    const int32_t cs[4] = {cf.x, cf.y, cf.z, cf.w};
+    uint32_t u[NB][8];
+#pragma unroll
+    for (int e = 0; e < NB; e++) gather_hint<8>(xs + (size_t)ws[e] * SW, u[e], gpol);
+#pragma unroll
+    for (int e = 0; e < NB; e++) {
+      const int32_t c = cs[e];
+      S += c;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int64_t p = (int64_t)c * (int64_t)(int32_t)u[e][i];
+        acc[i] += (int64_t)(uint32_t)p;
+        acc[i + 1] += (int64_t)(int32_t)(p >> 32);
+      }
+    }
+  }
+  // ---- normalise the slice: bias (see finalize), local carries
+  const int64_t b_lo = (S & 1) << 31, b_hi = S >> 1;
+  uint32_t wv[8];
+  int64_t carry = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int g = 8 * sl + i;
+    int64_t t = acc[i] + carry;
+    if (g < L) t += b_lo;
+    if (g >= 1 && g <= L) t += b_hi;
+    wv[i] = (uint32_t)t;
+    carry = t >> 32;
+  }
+  carry += acc[8];  // word 8 (sl + 1): the next slice's word 0
+  if (sl == T - 1 && 8 * T <= L) carry += b_hi;  // the top lane owns word 8T itself
+  // ---- carries up the row: after round r, slice r holds its final words
+#pragma unroll
+  for (int r = 1; r < T; r++) {
+    const int64_t cin = __shfl_up_sync(0xffffffffu, carry, 1);
+    if (sl == r) {
+      int64_t c = cin;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int64_t t = (int64_t)wv[i] + c;
+        wv[i] = (uint32_t)t;
+        c = t >> 32;
+      }
+      carry += c;
+    }
+  }
+  // ---- the row's first lane collects the words and finishes the row
+  uint32_t W[SW];
+#pragma unroll
+  for (int i = 0; i < 8; i++) W[i] = wv[i];
+#pragma unroll
+  for (int q = 1; q < T; q++)
+#pragma unroll
+    for (int i = 0; i < 8; i++) W[8 * q + i] = __shfl_down_sync(0xffffffffu, wv[i], q);
+  const int64_t top = __shfl_down_sync(0xffffffffu, carry, T - 1);  // value of words >= 8T
+  if (sl != 0 || !active) return;
+  int64_t acc2[L + 1];
+#pragma unroll
+  for (int i = 0; i < L; i++) acc2[i] = W[i];
+  {
+    uint64_t hi = (uint64_t)top;  // value of words >= L, fits int64 by the row bound
+#pragma unroll
+    for (int k = SW - 1; k >= L; k--) hi = (hi << 32) + W[k];
+    acc2[L] = (int64_t)hi;
+  }
+  if (!FIRST) {
+    uint32_t pin[SW];
+    load_slot<SW>(a.part_in + (size_t)slot * SW, pin, pol);
+#pragma unroll
+    for (int i = 0; i < L; i++) acc2[i] += pin[i];
+  }
+  if (LAST && a.has_full) row_full<L, 1>(a, mp, slot, a.slot_row[slot], a.x, acc2);
+  uint32_t Rr[L];
+  finalize<L>(acc2, 0, mp, Rr);
+  store_row<L, 1, LAST>(a, slot, 0, Rr, pol);
+}
+
 // ------------------------------------------------- die-split SpMV pass
 //
 // B200 is two dies, and each die's L2 keeps its own copy of every line its
@@ -484,11 +660,11 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
 //    context creation) and warps take slices from that die's work queue,
 //    then steal from the other queue once theirs is empty (correctness
 //    never depends on where CTAs land);
-//  * the two partial results of a row meet through an exchange buffer: each
-//    half stores its canonical value, fences, and bumps the slice's arrival
-//    counter; the second to arrive (odd count) adds the other's value mod
-//    ell and writes the row.  Counters grow by 2 per pass, so parity marks
-//    the order without ever being reset;
+//  * the two partial results of a row meet through an exchange buffer: the
+//    first half to finish a slice (per-slice arrival counter) publishes its
+//    canonical values there; the second adds them mod ell and writes the
+//    rows.  Counters grow by 4 per pass, so their residue mod 4 marks the
+//    order without ever being reset;
 //  * half 0 also carries the previous pass's partial and, on the last pass,
 //    the full-class entries and dense columns;
 //  * the last warp to leave resets the work queues for the next launch.
@@ -539,14 +715,11 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_split(const Sp
   const uint32_t* xc = a.x + (size_t)chain * SW;
   const int home = a.die_map[sm_id() & 255];
   const uint32_t nsl = (uint32_t)a.nslices;
-  const size_t xstride = (size_t)a.nslots * G * SW;
 #pragma unroll 1
   for (int pass_h = 0; pass_h < 2; pass_h++) {
     const int h = home ^ pass_h;  // own die's queue first, then help the other
     const SliceInfo* slices = a.slices + (size_t)h * a.nslices;
     const uint32_t* lk = a.lane_k4 + (size_t)h * a.nslots;
-    uint32_t* xmine = a.xch + (size_t)h * xstride;
-    const uint32_t* xother = a.xch + (size_t)(h ^ 1) * xstride;
 #pragma unroll 1
     while (true) {
       uint32_t base = 0;
@@ -573,31 +746,44 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_split(const Sp
         }
         uint32_t Rr[L];
         finalize<L>(acc, S, mp, Rr);
-        // publish this half's value, then count the arrival
-        {
+        // meet the other half: arrival counter +1 each, +2 when the first
+        // has published its value, so it grows by 4 per pass and
+        //   old % 4 == 0: first -> publish, signal
+        //   old % 4 == 3: second, value already published
+        //   old % 4 == 1: second, first still publishing (a few hundred
+        //                 cycles: it has finished its rows) -> wait
+        uint32_t old = 0;
+        if (lane == 0) old = atomicAdd(a.cnt + slice, 1u);
+        old = __shfl_sync(0xffffffffu, old, 0) & 3u;
+        uint32_t* xs = a.xch + ((size_t)slot * G + chain) * SW;
+        if (old == 0) {
           uint32_t o[SW];
 #pragma unroll
           for (int i = 0; i < SW; i++) o[i] = i < L ? Rr[i] : 0u;
-          store_slot<SW>(xmine + ((size_t)slot * G + chain) * SW, o);
-        }
-        // (the grid-barrier pattern: warp barrier, then one fenced atomic)
-        __syncwarp();
-        uint32_t old = 0;
-        if (lane == 0) {
-          __threadfence();
-          old = atomicAdd(a.cnt + slice, 1u);
-          if (old & 1u) __threadfence();
-        }
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (old & 1u) {  // second to arrive: combine and write the row
+          store_slot<SW>(xs, o);
+          __syncwarp();  // (the grid-barrier pattern: warp barrier, one fenced atomic)
+          if (lane == 0) {
+            __threadfence();
+            atomicAdd(a.cnt + slice, 2u);
+          }
+        } else {
+          if (lane == 0) {
+            if (old == 1) {
+              uint32_t c;
+              do {
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(a.cnt + slice) : "memory");
+              } while (c & 3u);
+            }
+            __threadfence();
+          }
+          __syncwarp();
           uint32_t pv[SW], P[L];
-          const uint32_t* src = xother + ((size_t)slot * G + chain) * SW;
 #pragma unroll
           for (int q = 0; q < SW / 8; q++)
             asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                          : "=r"(pv[8 * q + 0]), "=r"(pv[8 * q + 1]), "=r"(pv[8 * q + 2]), "=r"(pv[8 * q + 3]),
                            "=r"(pv[8 * q + 4]), "=r"(pv[8 * q + 5]), "=r"(pv[8 * q + 6]), "=r"(pv[8 * q + 7])
-                         : "l"(src + 8 * q)
+                         : "l"(xs + 8 * q)
                          : "memory");
 #pragma unroll
           for (int i = 0; i < L; i++) P[i] = pv[i];

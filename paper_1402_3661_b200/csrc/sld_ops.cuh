@@ -22,6 +22,8 @@ struct LOps {
                 const ModParams& mp);
   // resident CTAs per SM of the die-split kernel for G chains (0: unsupported)
   int (*split_occupancy)(int G);
+  // limb-sliced pass for one chain (false: L <= 8, no slicing)
+  bool (*wide)(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a, const ModParams& mp);
   void (*limbs_to_slots)(const uint32_t*, int64_t, uint32_t*, uint32_t, int64_t, int, cudaStream_t);
   void (*slots_to_limbs)(const uint32_t*, int64_t, uint32_t*, uint32_t, int64_t, int, cudaStream_t);
   void (*to_mont)(uint32_t*, int64_t, const ModParams&, cudaStream_t);
@@ -112,6 +114,19 @@ struct Ops {
       if (G == 4) return split_occ<L, 4>();
     return 0;
   }
+  static bool wide(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
+                   const ModParams& mp) {
+    if constexpr (wide_T<L>() >= 2) {
+      const unsigned grid = blocks_for(nslices * 32, 256);
+      if (!grid) return true;
+      if (first && last) spmv_wide<L, true, true><<<grid, 256, 0, s>>>(a, mp);
+      else if (first) spmv_wide<L, true, false><<<grid, 256, 0, s>>>(a, mp);
+      else if (last) spmv_wide<L, false, true><<<grid, 256, 0, s>>>(a, mp);
+      else spmv_wide<L, false, false><<<grid, 256, 0, s>>>(a, mp);
+      return true;
+    }
+    return false;
+  }
   static void l2s(const uint32_t* l, int64_t n, uint32_t* o, uint32_t b, int64_t rows, int G,
                   cudaStream_t s) {
     if (n) limbs_to_slots<L><<<blocks_for(n, 256), 256, 0, s>>>(l, n, o, b, rows, G);
@@ -139,7 +154,7 @@ struct Ops {
   static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
     if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);
   }
-  static LOps make() { return LOps{pass, split, split_occupancy, l2s, s2l, mont, zero, dproj, addm, rrows, lcomb, nz}; }
+  static LOps make() { return LOps{pass, split, split_occupancy, wide, l2s, s2l, mont, zero, dproj, addm, rrows, lcomb, nz}; }
 };
 
 template <int L, int LMIN>
