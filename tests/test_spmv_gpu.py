@@ -188,7 +188,7 @@ def test_die_split_vs_oracle(chains, stripe):
         pytest.skip("die map unavailable on this device")
     rng = np.random.default_rng(11 + chains)
     mod = PrimeModulus(2**200 - 75)
-    A = rand_matrix(mod, rng, 400, 380, 30, dense=1, full_frac=0.03)
+    A = rand_matrix(mod, rng, 400, 399, 30, dense=1, full_frac=0.03)  # square: iterate
     ys = [mod.random_residues(rng, A.total_cols) for _ in range(chains)]
     orc = to_oracle(A)
     P = digit_count(mod.ell)
