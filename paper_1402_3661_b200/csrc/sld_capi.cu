@@ -914,7 +914,21 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     stripe = std::max<int64_t>(1, stripe);
   }
   if (stripe >= ncols) stripe = std::max<int64_t>(ncols, 1);
-  const int npass = (int)std::max<int64_t>(1, (ncols + stripe - 1) / stripe);
+  // stripe boundaries: equal widths, or explicit ones (SLD_STRIPE_BOUNDS =
+  // "b1,b2,..." column indices, for layout sweeps)
+  std::vector<int64_t> bounds;
+  for (int64_t b = stripe; b < ncols; b += stripe) bounds.push_back(b);
+  if (const char* e = getenv("SLD_STRIPE_BOUNDS")) {
+    bounds.clear();
+    for (const char* q = e; *q;) {
+      char* end = nullptr;
+      const long long b = strtoll(q, &end, 10);
+      if (end == q) break;
+      if (b > 0 && b < ncols && (bounds.empty() || b > bounds.back())) bounds.push_back(b);
+      q = *end ? end + 1 : end;
+    }
+  }
+  const int npass = (int)bounds.size() + 1;
   M->npass = npass;
   M->stripe_cols = stripe;
   M->halves = H;
@@ -932,7 +946,10 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     const int64_t k = col / HC;
     return (((k + 1) * dn0) / dn - (k * dn0) / dn) ? 0 : 1;
   };
-  auto part_of = [&](int64_t col) -> int { return (int)(col / stripe) * H + half_of(col); };
+  auto part_of = [&](int64_t col) -> int {
+    const int pass = (int)(std::upper_bound(bounds.begin(), bounds.end(), col) - bounds.begin());
+    return pass * H + half_of(col);
+  };
   const int npart = npass * H;
   // ---- per-row, per-pass class counts
   RowCounts rc;

@@ -24,16 +24,18 @@ def main():
     ap.add_argument("--chains", default="1", help="comma list of chains per matrix pass")
     ap.add_argument("--split", default="", help="comma list of SLD_SPLIT values (die split off/on)")
     ap.add_argument("--frac", default="", help="comma list of SLD_SPLIT_FRAC values")
+    ap.add_argument("--bounds", default="", help="semicolon list of SLD_STRIPE_BOUNDS values")
     ap.add_argument("--pf", default="", help="comma list of SLD_PF values (index prefetch distance)")
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
     y = _random_residue_limbs(np.random.default_rng(5), A.total_cols, mod)
-    splits = [(sp, fr, pf) for sp in (a.split.split(",") if a.split else [""])
+    splits = [(sp, fr, pf, bd) for sp in (a.split.split(",") if a.split else [""])
               for fr in (a.frac.split(",") if a.frac else [""])
-              for pf in (a.pf.split(",") if a.pf else [""])]
-    for G, (sp, fr, pf) in [(int(x), s) for x in a.chains.split(",") for s in splits]:
-      for k, val in (("SLD_SPLIT", sp), ("SLD_SPLIT_FRAC", fr), ("SLD_PF", pf)):
+              for pf in (a.pf.split(",") if a.pf else [""])
+              for bd in (a.bounds.split(";") if a.bounds else [""])]
+    for G, (sp, fr, pf, bd) in [(int(x), s) for x in a.chains.split(",") for s in splits]:
+      for k, val in (("SLD_SPLIT", sp), ("SLD_SPLIT_FRAC", fr), ("SLD_PF", pf), ("SLD_STRIPE_BOUNDS", bd)):
           if val:
               os.environ[k] = val
           else:
@@ -58,7 +60,7 @@ def main():
                                   "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
             inf = dm.info()
             print(f"{a.config} G={G} stripes={inf['stripes']} halves={inf['halves']} split_frac={fr or '-'} "
-                  f"pf={pf or '-'} policy={pol} apw={apw}: "
+                  f"pf={pf or '-'} bounds={bd or '-'} policy={pol} apw={apw}: "
                   f"{per:.4f} ms/pass = {per / G:.4f} ms per chain-product  [{clk}]",
                   flush=True)
             v.close()
