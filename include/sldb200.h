@@ -42,6 +42,9 @@ extern "C" {
 #define SLD_E_BOUND -3   /* exactness bound exceeded (reference: AssertionError,
                             vecops.py:407,414 / ContractViolation modring.py:40) */
 #define SLD_E_NCCL -4    /* collective failure                                 */
+#define SLD_E_FORMAT -5  /* malformed file     (reference: fileio.FormatError)    */
+#define SLD_E_MAGIC -6   /* wrong magic bytes  (reference: fileio.BadMagic)       */
+#define SLD_E_TRUNC -7   /* file ends early    (reference: fileio.TruncatedFile)  */
 
 typedef struct sld_ctx sld_ctx;
 typedef struct sld_mat sld_mat;
@@ -206,6 +209,41 @@ int sld_corpus_rows(int64_t n, int64_t ncols, double gamma, uint64_t seed, int64
 int sld_corpus_fill(int64_t n, int64_t ncols, double decay, double pm1, int64_t cmax,
                     uint64_t seed, const int64_t *row_ptr, int32_t *col_idx, uint8_t *tags,
                     int64_t *small_vals, int nthreads);
+
+/*
+ * Native file formats of the reference (host code, no device needed).
+ *
+ * SLDM matrix (sldlag/spmatrix.py:14-22, store_matrix/load_matrix 358-436).
+ * sld_sldm_info scans the file (header_only: stops after the modulus, which
+ * the caller validates first, like the reference): info[0..7] = nrows, ncols, ell byte width,
+ * dense column count, nnz, full-class entries after re-classification, file
+ * bytes, ell limbs; ell_be receives the modulus big-endian (ell_cap >= width).
+ * sld_sldm_read fills the CSR arrays of SparseMatrix (row_ptr[nrows+1],
+ * col_idx[nnz], tags[nnz], small_vals[nnz], full_pos/full_limbs[n_full][L],
+ * dense_idx[dc], dense_limbs[dc][nrows][L]) re-classifying each coefficient
+ * to its smallest class like load_matrix.  sld_sldm_write emits the
+ * reference's exact bytes (atomic temp + fsync + rename).
+ */
+int sld_sldm_info(const char *path, int header_only, int64_t *info, uint8_t *ell_be, int ell_cap);
+int sld_sldm_read(const char *path, int L, int64_t *row_ptr, int32_t *col_idx, uint8_t *tags,
+                  int64_t *small_vals, int64_t *full_pos, uint32_t *full_limbs,
+                  int64_t *dense_idx, uint32_t *dense_limbs);
+int sld_sldm_write(const char *path, int64_t nrows, int64_t ncols, const uint32_t *ell, int L,
+                   const int64_t *row_ptr, const int32_t *col_idx, const uint8_t *tags,
+                   const int64_t *small_vals, int64_t n_full, const int64_t *full_pos,
+                   const uint32_t *full_limbs, int n_dense, const int64_t *dense_idx,
+                   const uint32_t *dense_limbs);
+/*
+ * SLDV vector (kind 0; spmatrix.py:24-25, store_vector/load_vector 439-462)
+ * and SLDQ Krylov terms (kind 1; checkpoint.py:11-14, store_terms/load_terms
+ * 36-64: count x m residues).  Residues cross as `stride` 32-bit limbs each.
+ * info[0..5] = kind, ell byte width, ell limbs, m (1 for SLDV), count,
+ * residues.
+ */
+int sld_sldv_write(const char *path, int kind, const uint32_t *ell, int L, int64_t m, int64_t count,
+                   const uint32_t *limbs, int stride);
+int sld_sldv_info(const char *path, int header_only, int64_t *info, uint8_t *ell_be, int ell_cap);
+int sld_sldv_read(const char *path, uint32_t *limbs, int stride);
 
 #ifdef __cplusplus
 }

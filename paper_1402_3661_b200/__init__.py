@@ -12,7 +12,12 @@ from .modring import (
     ints_to_limbs, ints_to_planes, limbs_to_ints, limbs_to_planes, planes_to_ints,
     planes_to_limbs,
 )
-from .spmatrix import DeviceKernel, SparseMatrix, classify, spmv_planes, spmv_sequential
+from .spmatrix import (
+    DeviceKernel, SparseMatrix, classify, load_matrix, load_vector, spmv_planes, spmv_sequential,
+    store_matrix, store_vector,
+)
+from .fileio import BadMagic, FormatError, TruncatedFile
+from .checkpoint import CHECKPOINT_EVERY, CheckpointManager, HaltRequested, load_terms, store_terms
 from .solver import (
     B200ChainGroup, B200Multiplier, BlockingParams, BlockSequence, DenseRows, SequentialMultiplier, UnitRows,
     draw_blocks, krylov_block, krylov_column, krylov_length, krylov_scalar,

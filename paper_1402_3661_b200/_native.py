@@ -19,6 +19,9 @@ SLD_E_ARG = -1
 SLD_E_CUDA = -2
 SLD_E_BOUND = -3
 SLD_E_NCCL = -4
+SLD_E_FORMAT = -5
+SLD_E_MAGIC = -6
+SLD_E_TRUNC = -7
 
 # every symbol include/sldb200.h declares (checked by tests/test_native_abi.py)
 EXPORTS = [
@@ -31,6 +34,7 @@ EXPORTS = [
     "sld_spmv", "sld_spmv_planes", "sld_krylov_unit",
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
     "sld_bench_spmv", "sld_corpus_rows", "sld_corpus_fill",
+    "sld_sldm_info", "sld_sldm_read", "sld_sldm_write", "sld_sldv_write", "sld_sldv_info", "sld_sldv_read",
 ]
 
 
@@ -95,6 +99,13 @@ def load(build_if_missing=False):
             "sld_xblock_destroy": ([vp], i32),
             "sld_krylov_dense": ([vp, vp, vp, i64, vp], i32),
             "sld_bench_spmv": ([vp, vp, i64, i32, vp, vp], i32),
+            "sld_sldm_info": ([ctypes.c_char_p, i32, vp, vp, i32], i32),
+            "sld_sldm_read": ([ctypes.c_char_p, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+            "sld_sldm_write": ([ctypes.c_char_p, i64, i64, vp, i32, vp, vp, vp, vp, i64, vp, vp, i32, vp, vp],
+                               i32),
+            "sld_sldv_write": ([ctypes.c_char_p, i32, vp, i32, i64, i64, vp, i32], i32),
+            "sld_sldv_info": ([ctypes.c_char_p, i32, vp, vp, i32], i32),
+            "sld_sldv_read": ([ctypes.c_char_p, vp, i32], i32),
             "sld_corpus_rows": ([i64, i64, ctypes.c_double, ctypes.c_uint64, vp], i32),
             "sld_corpus_fill": ([i64, i64, ctypes.c_double, ctypes.c_double, i64, ctypes.c_uint64,
                                  vp, vp, vp, vp, i32], i32),

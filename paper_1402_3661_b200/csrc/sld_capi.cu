@@ -50,6 +50,8 @@ static int fail(int code, const char* fmt, ...) {
   } while (0)
 
 extern "C" const char* sld_last_error(void) { return g_err.c_str(); }
+// error reporting for the host-only translation units (sld_fileio.cpp)
+int sld_set_error(int code, const char* msg) { return fail(code, "%s", msg); }
 extern "C" int sld_version(void) { return 1; }
 extern "C" int sld_device_count(int* out) {
   CU(cudaGetDeviceCount(out));

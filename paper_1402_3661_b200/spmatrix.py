@@ -237,3 +237,123 @@ def spmv_sequential(A, u, device=None) -> list:
         raise ValueError(f"vector length {len(u)} != {total_cols(A)} columns")
     planes = ints_to_planes(u, digit_count(A.mod.ell))
     return planes_to_ints(_kernel_of(A, device).apply(planes))
+
+
+# ------------------------------------------------------------ file formats
+# SLDM matrices and SLDV vectors (sldlag/spmatrix.py:14-25, 358-462), read
+# and written natively (csrc/sld_fileio.cpp): same bytes, same exception types.
+
+def _ell_from_be(buf, width):
+    from .fileio import FormatError
+    from .modring import PrimeModulus
+    ell = int.from_bytes(bytes(buf[:width]), "big")
+    try:
+        return PrimeModulus(ell)
+    except ValueError as e:
+        raise FormatError(str(e)) from e
+
+
+def _path(p):
+    import os
+    return os.fsencode(os.fspath(p))
+
+
+def store_matrix(A, path):
+    """Write A as SLDM (byte-identical to the reference's store_matrix)."""
+    from . import _native as N
+    from .device import matrix_arrays
+    from .fileio import check_io
+    mod = as_modulus(A.mod)
+    L = mod.limbs
+    row_ptr, col, tags, small, fpos, flimbs, n_dense, dense = matrix_arrays(A, L)
+    ell = np.asarray([(mod.ell >> (32 * i)) & 0xFFFFFFFF for i in range(L)], dtype=np.uint32)
+    didx = np.arange(A.ncols, A.ncols + n_dense, dtype=np.int64)
+    check_io(N.load().sld_sldm_write(
+        _path(path), int(A.nrows), int(A.ncols), N.ptr(ell), L, N.ptr(row_ptr), N.ptr(col),
+        N.ptr(tags), N.ptr(small), len(fpos), N.ptr(fpos), N.ptr(flimbs), n_dense, N.ptr(didx),
+        N.ptr(dense) if dense is not None else None))
+
+
+def load_matrix(path, dense_as_limbs=False):
+    """Read an SLDM file (the reference's load_matrix): coefficients are
+    re-classified to their smallest class; FormatError / BadMagic /
+    TruncatedFile / ValueError as the reference raises them.  Dense columns
+    come back as lists of ints, or as (nrows, L) limb arrays (no per-value
+    Python objects at NFS scale) with dense_as_limbs=True."""
+    from . import _native as N
+    from .fileio import check_io
+    from .modring import limbs_to_ints
+    info = np.zeros(8, dtype=np.int64)
+    ell_be = np.zeros(160, dtype=np.uint8)
+    check_io(N.load().sld_sldm_info(_path(path), 1, N.ptr(info), N.ptr(ell_be), len(ell_be)))
+    mod = _ell_from_be(ell_be, int(info[2]))
+    check_io(N.load().sld_sldm_info(_path(path), 0, N.ptr(info), N.ptr(ell_be), len(ell_be)))
+    nrows, ncols, eb, dc, nnz, nfull = (int(x) for x in info[:6])
+    L = mod.limbs
+    row_ptr = np.zeros(nrows + 1, dtype=np.int64)
+    col = np.zeros(max(nnz, 1), dtype=np.int32)
+    tags = np.zeros(max(nnz, 1), dtype=np.uint8)
+    small = np.zeros(max(nnz, 1), dtype=np.int64)
+    fpos = np.zeros(max(nfull, 1), dtype=np.int64)
+    flimbs = np.zeros((max(nfull, 1), L), dtype=np.uint32)
+    didx = np.zeros(max(dc, 1), dtype=np.int64)
+    dlimbs = np.zeros((max(dc, 1), nrows, L), dtype=np.uint32)
+    check_io(N.load().sld_sldm_read(_path(path), L, N.ptr(row_ptr), N.ptr(col), N.ptr(tags),
+                                    N.ptr(small), N.ptr(fpos), N.ptr(flimbs), N.ptr(didx),
+                                    N.ptr(dlimbs)))
+    fulls = dict(zip(fpos[:nfull].tolist(), limbs_to_ints(flimbs[:nfull]))) if nfull else {}
+    dense = []
+    for g in range(dc):
+        colv = dlimbs[g] if dense_as_limbs else limbs_to_ints(dlimbs[g])
+        dense.append((int(didx[g]), colv))
+    return SparseMatrix(mod, nrows, ncols, row_ptr, col[:nnz] if nnz else [],
+                        tags[:nnz], small[:nnz], fulls, dense)
+
+
+def _store_residues(path, kind, values, mod, m=1):
+    from . import _native as N
+    from .fileio import check_io
+    from .modring import ints_to_limbs
+    mod = as_modulus(mod)
+    L = mod.limbs
+    if isinstance(values, np.ndarray) and values.dtype == np.uint32 and values.ndim == 2:
+        limbs = np.ascontiguousarray(values)
+    else:
+        vals = list(values)
+        for v in vals:
+            mod.check(int(v))
+        limbs = ints_to_limbs(vals, L) if vals else np.zeros((0, L), dtype=np.uint32)
+    count = limbs.shape[0] // m if kind == 1 else limbs.shape[0]
+    ell = np.asarray([(mod.ell >> (32 * i)) & 0xFFFFFFFF for i in range(L)], dtype=np.uint32)
+    check_io(N.load().sld_sldv_write(_path(path), kind, N.ptr(ell), L, int(m), int(count),
+                                     N.ptr(limbs) if limbs.size else None, int(limbs.shape[1])))
+
+
+def _load_residues(path, want_kind):
+    from . import _native as N
+    from .fileio import BadMagic, check_io
+    info = np.zeros(6, dtype=np.int64)
+    ell_be = np.zeros(160, dtype=np.uint8)
+    check_io(N.load().sld_sldv_info(_path(path), 1, N.ptr(info), N.ptr(ell_be), len(ell_be)))
+    if int(info[0]) != want_kind:
+        raise BadMagic(f"{path}: magic {'SLDQ' if info[0] else 'SLDV'}, expected "
+                       f"{'SLDQ' if want_kind else 'SLDV'}")
+    mod = _ell_from_be(ell_be, int(info[1]))
+    check_io(N.load().sld_sldv_info(_path(path), 0, N.ptr(info), N.ptr(ell_be), len(ell_be)))
+    kind, eb, _, m, count, nres = (int(x) for x in info)
+    limbs = np.zeros((max(nres, 1), mod.limbs), dtype=np.uint32)
+    check_io(N.load().sld_sldv_read(_path(path), N.ptr(limbs), mod.limbs))
+    return limbs[:nres], mod, m, count
+
+
+def store_vector(vec, mod, path):
+    """SLDV vector of residues (ints, or an (n, L) uint32 limb array)."""
+    _store_residues(path, 0, vec, mod)
+
+
+def load_vector(path, as_limbs=False):
+    """Returns (vector, modulus) like the reference; as_limbs=True returns
+    the (n, L) uint32 limbs instead of Python ints."""
+    from .modring import limbs_to_ints
+    limbs, mod, _, _ = _load_residues(path, 0)
+    return (limbs if as_limbs else limbs_to_ints(limbs)), mod

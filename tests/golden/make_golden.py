@@ -291,6 +291,120 @@ def gen_mksol_cases():
     return out
 
 
+
+def gen_file_cases():
+    """SLDM / SLDV / SLDQ files written by the reference (store_matrix,
+    store_vector, store_terms) plus hand-framed SLDM files whose tags the
+    reference re-classifies on load, and malformed files with the exception
+    class the reference raises.  Files go to tests/golden/files/; the npz
+    holds what the reference's loaders return for each."""
+    import struct
+    from sldlag.checkpoint import store_terms
+    from sldlag.fileio import FormatError
+    from sldlag.spmatrix import load_matrix, store_matrix, store_vector
+    fdir = os.path.join(HERE, "files")
+    os.makedirs(fdir, exist_ok=True)
+    for f in os.listdir(fdir):
+        os.unlink(os.path.join(fdir, f))
+    d = {}
+    mats = [
+        ("m200", PrimeModulus(2**200 - 75), 300, 295, 12, 3, 0.1),
+        ("m1009", PrimeModulus(1009), 60, 60, 8, 1, 0.1),
+        ("m7", PrimeModulus(7), 40, 40, 6, 0, 0.1),
+        ("m650", PrimeModulus(int(gmpy2.next_prime(2**649 + 12345))), 80, 78, 10, 2, 0.3),
+        ("m61", PrimeModulus(2**61 - 1), 50, 50, 9, 0, 0.2),
+    ]
+    names = []
+    for name, mod, nr, nc, per, dense, ff in mats:
+        A = random_matrix(mod, np.random.default_rng(len(name) * 7 + nr), nr, nc, per, dense=dense,
+                          full_frac=ff)
+        store_matrix(A, os.path.join(fdir, name + ".sldm"))
+        d.update(matrix_arrays(name + "_", A))
+        names.append(name)
+    E = SparseMatrix.from_rows(PrimeModulus(1009), 0, 0, [])
+    store_matrix(E, os.path.join(fdir, "empty.sldm"))
+    d.update(matrix_arrays("empty_", E))
+    names.append("empty")
+    # hand-framed rows: +1 stored as small, small stored as full, -2^31 small
+    # (-> full), full payload 1 (-> +1), ell-1 as small payload (tiny ell)
+    def frame(mod, nrows, ncols, rows):
+        eb = mod.byte_width
+        out = [b"SLDM", struct.pack("<I", 1), struct.pack("<QQ", nrows, ncols),
+               struct.pack("<H", eb), mod.ell.to_bytes(eb, "big"), struct.pack("<I", 0)]
+        for r in rows:
+            out.append(struct.pack("<I", len(r)))
+            prev = 0
+            for c, tag, payload in r:
+                out.append(struct.pack("<QB", c - prev, tag))
+                prev = c
+                if tag == 2:
+                    out.append(struct.pack("<i", payload))
+                elif tag == 3:
+                    out.append(int(payload).to_bytes(eb, "little"))
+        return b"".join(out)
+    M200 = PrimeModulus(2**200 - 75)
+    M7 = PrimeModulus(7)
+    M199 = PrimeModulus(int(gmpy2.next_prime(2**199)))
+    reclass = {
+        "rc200": (M200, 3, 10, [[(0, 2, 1), (3, 2, -1), (5, 3, 12345), (9, 2, -2**31)],
+                                 [(1, 3, 1), (2, 3, M200.ell - 1), (4, 3, M200.ell - 2**31 + 1),
+                                  (8, 3, 2**31 + 5)],
+                                 [(0, 0, 0), (7, 1, 0), (9, 3, M200.ell - 2**40)]]),
+        "rc7": (M7, 2, 6, [[(0, 2, 6), (1, 2, -6), (2, 2, 13), (5, 3, 3)], [(4, 2, -2**31)]]),
+    }
+    for name, (mod, nr, nc, rows) in reclass.items():
+        with open(os.path.join(fdir, name + ".sldm"), "wb") as f:
+            f.write(frame(mod, nr, nc, rows))
+        A = load_matrix(os.path.join(fdir, name + ".sldm"))
+        d.update(matrix_arrays(name + "_", A))
+        names.append(name)
+    # malformed files and the reference's verdict
+    good = open(os.path.join(fdir, "m1009.sldm"), "rb").read()
+    bad = {
+        "bad_magic": b"XXXX" + good[4:],
+        "bad_trunc": good[:-3],
+        "bad_trailing": good + b"\0",
+        "bad_version": good[:4] + struct.pack("<I", 2) + good[8:],
+        "bad_tag": frame(M7, 1, 4, [[(0, 7, 0)]]),
+        "bad_zero": frame(M7, 1, 4, [[(1, 2, 14)]]),
+        "bad_zero_full": frame(M7, 1, 4, [[(1, 3, 0)]]),
+        "bad_col": frame(M7, 1, 4, [[(5, 0, 0)]]),
+        "bad_noncanon": frame(M199, 1, 4, [[(1, 3, M199.ell + 2**198)]]),
+        "ok_noncanon_small": frame(M200, 1, 4, [[(1, 3, M200.ell + 10)]]),
+        "bad_ell": frame(M7, 1, 4, [])[:24] + struct.pack("<H", 1) + bytes([9]) + frame(M7, 1, 4, [])[27:],
+    }
+    verdicts = []
+    for name, blob in bad.items():
+        path = os.path.join(fdir, name + ".sldm")
+        with open(path, "wb") as f:
+            f.write(blob)
+        try:
+            A = load_matrix(path)
+            verdicts.append("ok")
+            d.update(matrix_arrays(name + "_", A))
+        except FormatError as e:
+            verdicts.append(type(e).__name__)
+        except ValueError:
+            verdicts.append("ValueError")
+    d["bad_names"] = np.array(list(bad))
+    d["bad_verdicts"] = np.array(verdicts)
+    d["matrix_names"] = np.array(names)
+    # vectors and terms
+    rng = np.random.default_rng(9)
+    for name, mod, n in (("v200", M200, 77), ("v7", M7, 5), ("v650", mats[3][1], 33), ("v0", M200, 0)):
+        vec = mod.random_residues(rng, n)
+        store_vector(vec, mod, os.path.join(fdir, name + ".sldv"))
+        d[name + "_ell"] = np.array(hex(mod.ell))
+        d[name + "_vals"] = res_bytes(vec, mod.byte_width)
+    terms = [M200.random_residues(rng, 4) for _ in range(9)]
+    store_terms(os.path.join(fdir, "q200.sldq"), terms, 4, M200)
+    d["q200_vals"] = res_bytes([v for t in terms for v in t], M200.byte_width)
+    d["q200_m"] = np.array(4)
+    # the manifest of every file's bytes
+    for f in sorted(os.listdir(fdir)):
+        d["sha_" + f] = np.array(hashlib.sha256(open(os.path.join(fdir, f), "rb").read()).hexdigest())
+    return d
+
 def main():
     jobs = {
         "spmv_cases.npz": gen_spmv_cases,
@@ -298,6 +412,7 @@ def main():
         "grid_cases.npz": gen_grid_cases,
         "cfg1.npz": gen_cfg1,
         "mksol_cases.npz": gen_mksol_cases,
+        "file_cases.npz": gen_file_cases,
     }
     only = sys.argv[1:]
     manifest = []

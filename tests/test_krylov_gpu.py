@@ -198,3 +198,24 @@ def test_krylov_block_grouped_equals_ungrouped():
     two = krylov_block(A, X, Y, 45, chains_per_gpu=2)
     four = krylov_block(A, X, Y, 45, chains_per_gpu=4)
     assert one.columns == two.columns == four.columns
+
+
+def test_native_checkpoint_halt_and_resume(tmp_path):
+    # a device chain under the native CheckpointManager: halt after a flush,
+    # resume from the files, finish -- identical to the uninterrupted chain
+    from paper_1402_3661_b200 import CheckpointManager, HaltRequested
+    mod = PrimeModulus(2**200 - 75)
+    rng = np.random.default_rng(23)
+    A = rand_matrix(mod, rng, 64, 64, 7)
+    y = mod.random_residues(rng, 64)
+    P = digit_count(mod.ell)
+    X = UnitRows([0, 5])
+    full, vfull, _ = krylov_column(B200Multiplier(A), X, ints_to_planes(y, P), 50)
+    ck = CheckpointManager(tmp_path, mod, every=8, halt_after=19, async_writes=True)
+    ck.m = 2
+    with pytest.raises(HaltRequested):
+        krylov_column(B200Multiplier(A), X, ints_to_planes(y, P), 50, checkpoint=ck)
+    terms, v = CheckpointManager(tmp_path, mod).load_column(0)
+    assert len(terms) == 19 and terms == full[:19]
+    rest, vrest, n = krylov_column(B200Multiplier(A), X, v, 50, start_terms=terms)
+    assert n == 31 and rest == full and np.array_equal(vrest, vfull)
