@@ -1,0 +1,26 @@
+#!/bin/bash
+# One GPU session: tests, smoke, benches, ncu launch lists and one full
+# capture of the top kernel.  Output under gpurun_out/ (copied to profiles/
+# by hand once reviewed).  Usage: tools/gpu_round.sh [tag]
+TAG=${1:-r01}
+O=gpurun_out
+mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/gputests_$TAG.log 2>&1; echo "rc=$?" >> $O/gputests_$TAG.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke_$TAG.log 2>&1; echo "rc=$?" >> $O/smoke_$TAG.log
+for c in cfg3 cfg2 cfg5 cfg1; do
+  timeout 900 python bench.py --config $c > $O/bench_${c}_$TAG.json 2> $O/bench_${c}_$TAG.err
+done
+timeout 600 python bench.py --impl reference > $O/bench_ref_cfg3_$TAG.json 2> $O/bench_ref_cfg3_$TAG.err
+# launch lists (cold-cache, serialised: shares only) of the bench command
+timeout 900 ncu --graph-profiling node --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+  --clock-control none -k regex:spmv_ -c 40 --csv --log-file $O/launches_cfg3_$TAG.csv \
+  python bench.py --config cfg3 --steps 4 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+for c in cfg2:2 cfg5:1; do
+  timeout 600 ncu --graph-profiling node --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+    --clock-control none -k regex:spmv_ -c 12 --csv --log-file $O/launches_${c%%:*}_$TAG.csv \
+    python tools/profile_spmv.py --config ${c%%:*} --chains ${c##*:} --steps 6 > /dev/null 2>&1
+done
+# one full capture of the dominant kernel (first stripe pass at cfg3)
+timeout 900 ncu --set full --import-source on --graph-profiling node --clock-control none -k regex:spmv_pass -s 8 -c 1 \
+  -o $O/full_cfg3_$TAG python tools/profile_spmv.py --config cfg3 --chains 2 --steps 4 > /dev/null 2>&1
+tail -2 $O/gputests_$TAG.log; tail -1 $O/smoke_$TAG.log
