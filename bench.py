@@ -48,9 +48,10 @@ CONFIGS = {
 }
 DEFAULT_CONFIG = "cfg3"
 
-# measured random-gather rates from L2 (GB/s) for records of 1, 2, 4 sectors
-# fetched by one request (profiles/microbench_r01.txt, microbench2_r01.txt)
-L2_GATHER_PEAK_GBS = {1: 9200.0, 2: 15460.0, 4: 15000.0}
+# measured random-gather rates from L2 (GB/s) for records of 1-4 sectors
+# fetched by one instruction of 1-4 lanes (profiles/microbench_r01.txt,
+# microbench2_r01.txt; 96-byte records straddle 128-byte lines)
+L2_GATHER_PEAK_GBS = {1: 9200.0, 2: 15460.0, 3: 12880.0, 4: 16990.0}
 
 
 def dist_env():
@@ -455,7 +456,11 @@ def main():
         with open(tfile) as f:
             traffic = json.load(f).get("dram_bytes_per_pass")
     gather_bytes = G * 32 * ((4 * L + 31) // 32) * (Z + Zf) + B_pass
-    gpeak = L2_GATHER_PEAK_GBS[G]
+    # sectors one gather instruction fetches as one request: G chains x the
+    # lanes a residue is sliced over (wide moduli); otherwise a lane issues
+    # one request per sector and the 1-sector rate applies
+    rec_sectors = G * info.get("lanes_per_residue", 1)
+    gpeak = L2_GATHER_PEAK_GBS[rec_sectors]
     line = {
         "metric": METRIC, "value": value, "unit": "SpMV/s", "n_gpus": world, "steps": steps_even,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -469,6 +474,7 @@ def main():
                      "algorithmic_bytes_per_step": B_pass, "algorithmic_bytes_per_product": B,
                      "kernel": "spmv_pass (all stripe passes of one step)"},
         "gather_roofline": {"bound": "l2_random_gather_requests", "peak": gpeak,
+                            "sectors_per_request": rec_sectors,
                             "unit": "GB/s", "bytes_per_step": gather_bytes,
                             "achieved": gather_bytes / (ms_per_step / 1e3) / 1e9,
                             "frac": gather_bytes / (ms_per_step / 1e3) / 1e9 / gpeak},

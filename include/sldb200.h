@@ -108,10 +108,11 @@ int sld_mat_create_chains(sld_ctx *ctx, int chains, int64_t nrows, int64_t ncols
                           int n_dense, const uint32_t *dense_limbs,
                           int64_t max_stripe_cols, sld_mat **out);
 int sld_mat_destroy(sld_mat *m);
-/* info[0..15]: nrows, total_cols, nnz, n_pm, n_small, n_full(+dense nz),
+/* info[0..19]: nrows, total_cols, nnz, n_pm, n_small, n_full(+dense nz),
  * stripes, nslices, device bytes, padded index entries, L, stride words,
  * max row degree, stripe columns, chains, halves (2 = columns dealt to
- * the two dies, see sld_die_map) */
+ * the two dies, see sld_die_map), lanes per residue (limb-sliced passes:
+ * SW/8, else 1), rows per slice, index prefetch distance, 0 */
 int sld_mat_info(const sld_mat *m, int64_t *info);
 
 /*

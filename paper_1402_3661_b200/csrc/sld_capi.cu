@@ -1248,9 +1248,10 @@ extern "C" int sld_mat_create_chains(sld_ctx* ctx, int chains, int64_t nrows, in
 
 extern "C" int sld_mat_info(const sld_mat* m, int64_t* info) {
   if (!m || !info) return fail(SLD_E_ARG, "null argument");
-  int64_t v[16] = {m->nrows, m->total_cols, m->nnz, m->n_pm, m->n_small, m->n_full,
+  int64_t v[20] = {m->nrows, m->total_cols, m->nnz, m->n_pm, m->n_small, m->n_full,
                    m->npass, m->nslices, (int64_t)m->dev_bytes, m->pad_entries,
-                   m->ctx->L, m->ctx->SW, m->max_deg, m->stripe_cols, m->chains, m->halves};
+                   m->ctx->L, m->ctx->SW, m->max_deg, m->stripe_cols, m->chains, m->halves,
+                   m->sliced ? m->ctx->SW / 8 : 1, m->nslices ? m->nslots / m->nslices : 0, m->pf, 0};
   memcpy(info, v, sizeof(v));
   return SLD_OK;
 }

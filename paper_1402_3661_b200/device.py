@@ -188,7 +188,8 @@ class DeviceMatrix:
 
     INFO_KEYS = ("nrows", "total_cols", "nnz", "n_pm", "n_small", "n_full", "stripes",
                  "nslices", "device_bytes", "pad_entries", "L", "stride_words", "max_degree",
-                 "stripe_cols", "chains", "halves")
+                 "stripe_cols", "chains", "halves", "lanes_per_residue", "rows_per_slice",
+                 "prefetch")
 
     def __init__(self, A, device=None, stripe_cols=0, field=None, chains=1):
         self.mod = as_modulus(A.mod)
@@ -218,7 +219,7 @@ class DeviceMatrix:
         return self._h
 
     def info(self):
-        out = np.zeros(16, dtype=np.int64)
+        out = np.zeros(20, dtype=np.int64)
         N.check(N.load().sld_mat_info(self._h, N.ptr(out)))
         return {k: int(v) for k, v in zip(self.INFO_KEYS, out)}
 

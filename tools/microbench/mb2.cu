@@ -91,7 +91,7 @@ int main(){
     for(int r=0;r<4;r++){ cudaEventRecord(e0); seq_read<<<pr.multiProcessorCount*8,256>>>(buf,nw,reps,out); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms,e0,e1); if(r>0&&ms<best)best=ms;}
     printf("L2 sequential read ws=%3zu MB: %8.1f GB/s\n", mb, (double)nw*4*reps/best/1e6);
   }
-  for(int G : {1, 2, 4})
+  for(int G : {1, 2, 3, 4})
   for(size_t mb : {32, 64, 512}){
     uint32_t nrec = (uint32_t)((mb<<20)/(32*G)); uint32_t iters = 1024;
     int blocks = pr.multiProcessorCount*8;
@@ -99,6 +99,7 @@ int main(){
     for(int r=0;r<4;r++){ cudaEventRecord(e0);
       if(G==1) coop_gather<1><<<blocks,256>>>(buf,nrec,iters,r*3u,out);
       if(G==2) coop_gather<2><<<blocks,256>>>(buf,nrec,iters,r*3u,out);
+      if(G==3) coop_gather<3><<<blocks,256>>>(buf,nrec,iters,r*3u,out);
       if(G==4) coop_gather<4><<<blocks,256>>>(buf,nrec,iters,r*3u,out);
       cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms,e0,e1); if(r>0&&ms<best)best=ms;}
     double by = (double)blocks*256*iters*32;
