@@ -61,7 +61,7 @@ struct SpmvArgs {
   int64_t nslices;
   int64_t nslots;  // nslices * rows per slice (dense-value row stride)
   int has_full;
-  int policy;  // bit0 gather L2 evict_last, bit1 output store evict_first,
+  int policy;  // bit0 gather L2 evict_last, bit1 output store evict_first, bit4 exchange store evict_first,
                // bit2 partial store evict_first, bit3 gathers L1::no_allocate
   // die-split passes (spmv_split): slices / lane_k4 hold both halves, half h
   // at offset h * nslices / h * nslots
@@ -760,7 +760,8 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_split(const Sp
           uint32_t o[SW];
 #pragma unroll
           for (int i = 0; i < SW; i++) o[i] = i < L ? Rr[i] : 0u;
-          store_slot<SW>(xs, o);
+          if (a.policy & 16) store_slot_hint<SW>(xs, o, pol);
+          else store_slot<SW>(xs, o);
           __syncwarp();  // (the grid-barrier pattern: warp barrier, one fenced atomic)
           if (lane == 0) {
             __threadfence();
