@@ -373,6 +373,20 @@ static const DieMap* die_map(int dev, int sms) {
   return &d;
 }
 
+// the context's device copy of the die map, probed on first use (only the
+// opt-in die split needs it; the probe costs ~0.7 s once per process)
+static int ctx_dies(sld_ctx* c) {
+  if (c->die_map) return SLD_OK;
+  const DieMap* d = die_map(c->dev, c->sms);
+  CU(cudaMalloc(&c->die_map, 256));
+  CU(cudaMemcpy(c->die_map, d->map, 256, cudaMemcpyHostToDevice));
+  if (d->ok) {
+    c->die_n[0] = d->n[0];
+    c->die_n[1] = d->n[1];
+  }
+  return SLD_OK;
+}
+
 extern "C" int sld_die_map(int device, uint8_t* map256, int* n_die0, int* n_die1) {
   int ndev = 0;
   CU(cudaGetDeviceCount(&ndev));
@@ -468,15 +482,6 @@ extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pr.persistingL2CacheMaxSize);
   CU(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
-  {
-    const DieMap* d = die_map(device, c->sms);
-    CU(cudaMalloc(&c->die_map, 256));
-    CU(cudaMemcpy(c->die_map, d->map, 256, cudaMemcpyHostToDevice));
-    if (d->ok) {
-      c->die_n[0] = d->n[0];
-      c->die_n[1] = d->n[1];
-    }
-  }
   *out = c.release();
   return SLD_OK;
 }
@@ -892,6 +897,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     // 1.36 ms per chain-product), so the split is opt-in.
     int want = 0;
     if (const char* e = getenv("SLD_SPLIT")) want = atoi(e);
+    if (want && !M->sliced && nrows > 0) TRY(ctx_dies(c));
     if (want && !M->sliced && c->die_n[0] > 0 && c->die_n[1] > 0 && nrows > 0 &&
         ops(L).split_occupancy(M->chains) > 0)
       H = 2;
