@@ -147,7 +147,8 @@ struct sld_xblock {
   sld_ctx* ctx = nullptr;
   int m = 0;
   int64_t n = 0;
-  uint32_t* x = nullptr;  // [t][j] Montgomery form, SW stride
+  uint32_t* x = nullptr;     // [t][j] SW stride: plain (L <= 8, lazy dot products) or Montgomery form
+  uint32_t* fold = nullptr;  // L <= 8: 2^(32k) mod ell for k = L .. 2L (L words each)
 };
 
 struct sld_mat {
@@ -1505,10 +1506,22 @@ extern "C" int sld_xblock_create(sld_ctx* ctx, const uint32_t* x_limbs, int m, i
     CU(cudaMalloc(&d, cnt * ctx->L * 4));
     CU(cudaMemcpyAsync(d, x_limbs, cnt * ctx->L * 4, cudaMemcpyHostToDevice, ctx->stream));
     ops(ctx->L).limbs_to_slots(d, (int64_t)cnt, xb->x, 0u, (int64_t)cnt, 1, ctx->stream);
-    ops(ctx->L).to_mont(xb->x, (int64_t)cnt, ctx->mp, ctx->stream);
+    if (ctx->L > 8) ops(ctx->L).to_mont(xb->x, (int64_t)cnt, ctx->mp, ctx->stream);
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     cudaFree(d);
     if (e != cudaSuccess) return fail(SLD_E_CUDA, "x block upload: %s", cudaGetErrorString(e));
+  }
+  if (ctx->L <= 8) {
+    // 2^(32k) mod ell, k = L .. 2L, for the lazy dot products' final fold
+    const int L = ctx->L;
+    std::vector<uint32_t> r(L, 0), tab((size_t)(L + 1) * L);
+    r[0] = 1;
+    for (int k = 0; k <= 2 * L; k++) {
+      if (k >= L) std::copy(r.begin(), r.end(), tab.begin() + (size_t)(k - L) * L);
+      for (int b = 0; b < 32; b++) hmod_double(r.data(), ctx->mp.ell, L);
+    }
+    CU(cudaMalloc(&xb->fold, tab.size() * 4));
+    CU(cudaMemcpy(xb->fold, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
   }
   *out = xb.release();
   return SLD_OK;
@@ -1517,6 +1530,7 @@ extern "C" int sld_xblock_create(sld_ctx* ctx, const uint32_t* x_limbs, int m, i
 extern "C" int sld_xblock_destroy(sld_xblock* x) {
   if (!x) return SLD_OK;
   cudaSetDevice(x->ctx->dev);
+  if (x->fold) cudaFree(x->fold);
   if (x->x) cudaFree(x->x);
   delete x;
   return SLD_OK;
@@ -1545,6 +1559,7 @@ extern "C" int sld_krylov_dense(sld_mat* M, sld_vec* v, sld_xblock* X, int64_t s
   if (dense_proj_prepare(M->ctx->sms, m, v->n, c->SW, &M->dproj_part, &M->dproj_cap, &da))
     return fail(SLD_E_CUDA, "dense projection scratch allocation failed");
   da.x = X->x;
+  da.fold = X->fold;
   std::vector<uint32_t> tmp;
   int64_t done = 0;
   while (done < steps) {

@@ -83,6 +83,35 @@ def test_dense_x_vs_oracle():
     assert terms == [O.limbs_to_ints(t) for t in ot]
 
 
+@pytest.mark.parametrize("bits", [2, 31, 64, 127, 202, 256, 300, 650])
+@pytest.mark.parametrize("extreme", [False, True])
+def test_dense_x_widths_vs_oracle(bits, extreme):
+    # L <= 8: lazy exact dot products (16-bit digit x limb columns, one fold
+    # and Barrett per term); L > 8: Montgomery products.  extreme: x = v =
+    # l - 1 on a longer vector drives every column to its bound
+    from paper_1402_3661_b200.modring import next_prime
+    ell = 3 if bits == 2 else next_prime((1 << bits) - (1 << (bits // 2)))
+    if ell.bit_length() > bits:
+        ell = next_prime(1 << (bits - 1))
+    mod = PrimeModulus(ell)
+    rng = np.random.default_rng(bits + (7 if extreme else 0))
+    n = 3000 if extreme else 200
+    A = rand_matrix(mod, rng, n, n, 6)
+    if extreme:
+        y = [ell - 1] * n
+        xs = [[ell - 1] * n for _ in range(3)]
+    else:
+        y = mod.random_residues(rng, n)
+        xs = [mod.random_residues(rng, n) for _ in range(3)]
+    X = DenseRows(xs, mod)
+    orc = to_oracle(A)
+    x = np.stack([O.ints_to_limbs(v, mod.limbs) for v in xs])
+    ot, _ = O.krylov_dense(orc, O.ints_to_limbs(y, mod.limbs), x, 6)
+    terms, _, _ = krylov_column(B200Multiplier(A), X, ints_to_planes(y, digit_count(mod.ell)), 6)
+    assert terms == [O.limbs_to_ints(t) for t in ot]
+    assert terms[0] == [sum(a * b for a, b in zip(xv, y)) % ell for xv in xs]
+
+
 def test_krylov_scalar_identity_and_zero():
     mod = PrimeModulus(1009)
     rng = np.random.default_rng(1)
