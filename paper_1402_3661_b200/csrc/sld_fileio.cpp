@@ -330,37 +330,123 @@ struct SldmOut {
   int L;                 // limb stride of full_limbs
 };
 
-int sldm_rows(Cur& c, const SldmHead& h, int64_t* nnz_out, int64_t* nfull_out, const SldmOut* out) {
+// Rows are variable-length records, so the parse runs in two steps:
+//  1. a sequential skip-scan that only reads entry counts and tags (payload
+//     sizes) to find where every row starts, stopping at a structural error
+//     (truncation, unknown tag);
+//  2. a parallel parse of the rows before that point, one thread per row
+//     range; each thread keeps the first error of its range.
+// The error reported is the first one in file order, as the reference's
+// sequential loop would raise it.
+struct RowScan {
+  std::vector<uint64_t> off;  // byte offset of each row record
+  std::vector<int64_t> first; // first entry index of each row (nrows + 1)
+  int64_t good_rows = 0;      // rows before the structural error (all if none)
+  int err = SLD_OK;           // structural error after good_rows
+  std::string msg;
+  size_t end = 0;             // offset after the last row (no error)
+};
+
+int sldm_scan(Cur& c, const SldmHead& h, RowScan* rs) {
+  const int eb = h.ell.eb;
+  rs->off.assign(h.nrows + 1, 0);
+  rs->first.assign(h.nrows + 1, 0);
+  const uint8_t* p = c.p;
+  size_t pos = c.pos;
+  const size_t n = c.n;
+  int64_t nnz = 0;
+  for (int64_t r = 0; r < h.nrows; r++) {
+    rs->off[r] = pos;
+    rs->first[r] = nnz;
+    if (pos + 4 > n) {
+      rs->good_rows = r;
+      rs->err = ferr(SLD_E_TRUNC, "%s: needed 4 bytes at offset %zu, file has %zu", c.name, pos, n);
+      rs->msg = sld_last_error();
+      return SLD_OK;
+    }
+    uint32_t count;
+    memcpy(&count, p + pos, 4);
+    pos += 4;
+    for (uint32_t k = 0; k < count; k++) {
+      if (pos + 9 > n) {
+        rs->good_rows = r;
+        rs->err = ferr(SLD_E_TRUNC, "%s: needed 9 bytes at offset %zu, file has %zu", c.name, pos, n);
+        rs->msg = sld_last_error();
+        return SLD_OK;
+      }
+      const uint8_t tag = p[pos + 8];
+      pos += 9;
+      size_t pay = tag == 2 ? 4 : tag == 3 ? (size_t)eb : 0;
+      if (tag > 3) {
+        rs->good_rows = r;
+        rs->err = ferr(SLD_E_FORMAT, "unknown entry tag %u", tag);
+        rs->msg = sld_last_error();
+        return SLD_OK;
+      }
+      if (pos + pay > n) {
+        rs->good_rows = r;
+        rs->err = ferr(SLD_E_TRUNC, "%s: needed %zu bytes at offset %zu, file has %zu", c.name, pay, pos, n);
+        rs->msg = sld_last_error();
+        return SLD_OK;
+      }
+      pos += pay;
+    }
+    nnz += count;
+  }
+  rs->off[h.nrows] = pos;
+  rs->first[h.nrows] = nnz;
+  rs->good_rows = h.nrows;
+  rs->end = pos;
+  return SLD_OK;
+}
+
+struct RangeOut {
+  int err = SLD_OK;
+  int64_t err_row = -1;
+  std::string msg;
+  std::vector<int64_t> fpos;
+  std::vector<uint32_t> flimbs;
+};
+
+// parse rows [lo, hi); entries of a bad row before the error are written
+void parse_range(const uint8_t* base, const SldmHead& h, const RowScan& rs, int64_t lo, int64_t hi,
+                 const SldmOut* out, RangeOut* ro) {
   const Ell& e = h.ell;
   const int eb = e.eb, L = e.L;
   std::vector<uint32_t> v(L + 1);
-  int64_t nnz = 0, nfull = 0;
-  if (out) out->row_ptr[0] = 0;
-  for (int64_t r = 0; r < h.nrows; r++) {
+  auto bad = [&](int64_t r, int code, const char* m) {
+    ro->err = code;
+    ro->err_row = r;
+    ro->msg = m;
+  };
+  for (int64_t r = lo; r < hi; r++) {
+    const uint8_t* q = base + rs.off[r];
     uint32_t count;
-    TRYF(c.get(&count));
+    memcpy(&count, q, 4);
+    q += 4;
+    int64_t pidx = rs.first[r];
     uint64_t prev = 0;
-    for (uint32_t k = 0; k < count; k++) {
-      const uint8_t* q;
-      TRYF(c.take(9, &q));
+    for (uint32_t k = 0; k < count; k++, pidx++) {
       uint64_t delta;
       memcpy(&delta, q, 8);
       const uint8_t tag = q[8];
+      q += 9;
       const uint64_t col = prev + delta;
-      if (k > 0 && delta == 0)
-        return ferr(SLD_E_ARG, "column indices not strictly increasing within a row");
+      if (k > 0 && delta == 0) return bad(r, SLD_E_ARG, "column indices not strictly increasing within a row");
       prev = col;
       uint8_t t2;
       int64_t word;
       if (tag == 2) {
         int32_t x;
-        TRYF(c.get(&x));
-        if (!i32_residue(x, e, v.data())) return ferr(SLD_E_ARG, "zero coefficient in file");
+        memcpy(&x, q, 4);
+        q += 4;
+        if (!i32_residue(x, e, v.data())) return bad(r, SLD_E_ARG, "zero coefficient in file");
         classify(v.data(), e, &t2, &word);
       } else if (tag == 3) {
-        TRYF(c.take(eb, &q));
-        if (!le_fits(q, eb, L)) return ferr(SLD_E_ARG, "full coefficient is not a canonical residue");
         le_to_limbs(q, eb, v.data(), L);
+        const bool fits = le_fits(q, eb, L);
+        q += eb;
+        if (!fits) return bad(r, SLD_E_ARG, "full coefficient is not a canonical residue");
         // the reference classifies v mod ell but keeps v itself as the full
         // value, which must then be canonical (spmatrix.py:419-432)
         bool canonical = true;
@@ -370,35 +456,65 @@ int sldm_rows(Cur& c, const SldmHead& h, int64_t* nnz_out, int64_t* nfull_out, c
         }
         bool nz = false;
         for (int i = 0; i < L; i++) nz |= v[i] != 0;
-        if (!nz) return ferr(SLD_E_ARG, "zero coefficient in file");
+        if (!nz) return bad(r, SLD_E_ARG, "zero coefficient in file");
         classify(v.data(), e, &t2, &word);
-        if (t2 == 3 && !canonical) return ferr(SLD_E_ARG, "full coefficient is not a canonical residue");
+        if (t2 == 3 && !canonical) return bad(r, SLD_E_ARG, "full coefficient is not a canonical residue");
       } else if (tag == 0) {
         t2 = 0;
         word = 1;
-      } else if (tag == 1) {
-        // ell - 1 re-classifies to -1 (and to +1 only for ell = 2, excluded)
+      } else {
+        // tag 1 (the scan rejected tags > 3): ell - 1 re-classifies to -1
         t2 = 1;
         word = -1;
-      } else {
-        return ferr(SLD_E_FORMAT, "unknown entry tag %u", tag);
       }
-      if (col >= (uint64_t)h.ncols) return ferr(SLD_E_ARG, "sparse column index out of range");
+      if (col >= (uint64_t)h.ncols) return bad(r, SLD_E_ARG, "sparse column index out of range");
       if (out) {
-        out->col_idx[nnz] = (int32_t)col;
-        out->tags[nnz] = t2;
-        out->small_vals[nnz] = word;
-        if (t2 == 3) {
-          out->full_pos[nfull] = nnz;
-          memcpy(out->full_limbs + (size_t)nfull * out->L, v.data(), sizeof(uint32_t) * std::min(L, out->L));
-        }
+        out->col_idx[pidx] = (int32_t)col;
+        out->tags[pidx] = t2;
+        out->small_vals[pidx] = word;
       }
-      nfull += t2 == 3;
-      nnz++;
+      if (t2 == 3) {
+        ro->fpos.push_back(pidx);
+        if (out) ro->flimbs.insert(ro->flimbs.end(), v.begin(), v.begin() + L);
+      }
     }
-    if (out) out->row_ptr[r + 1] = nnz;
   }
-  *nnz_out = nnz;
+}
+
+// scan + parallel parse; returns the first error in file order
+int sldm_rows(Cur& c, const SldmHead& h, int64_t* nnz_out, int64_t* nfull_out, const SldmOut* out) {
+  RowScan rs;
+  TRYF(sldm_scan(c, h, &rs));
+  const int64_t nr = rs.good_rows;
+  const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const int parts = nr < 4096 ? 1 : nt;
+  std::vector<RangeOut> ro(parts);
+  std::vector<std::thread> th;
+  const int64_t chunk = (nr + parts - 1) / std::max(parts, 1);
+  for (int t = 0; t < parts; t++) {
+    const int64_t lo = t * chunk, hi = std::min<int64_t>(nr, lo + chunk);
+    if (lo >= hi) break;
+    if (parts == 1) parse_range(c.p, h, rs, lo, hi, out, &ro[t]);
+    else th.emplace_back([&, lo, hi, t] { parse_range(c.p, h, rs, lo, hi, out, &ro[t]); });
+  }
+  for (auto& x : th) x.join();
+  for (auto& r : ro)
+    if (r.err != SLD_OK) return sld_set_error(r.err, r.msg.c_str());
+  if (rs.err != SLD_OK) return sld_set_error(rs.err, rs.msg.c_str());
+  int64_t nfull = 0;
+  for (auto& r : ro) {
+    if (out)
+      for (size_t k = 0; k < r.fpos.size(); k++) {
+        out->full_pos[nfull + (int64_t)k] = r.fpos[k];
+        memcpy(out->full_limbs + (size_t)(nfull + (int64_t)k) * out->L, r.flimbs.data() + k * h.ell.L,
+               sizeof(uint32_t) * std::min(h.ell.L, out->L));
+      }
+    nfull += (int64_t)r.fpos.size();
+  }
+  if (out)
+    for (int64_t r = 0; r <= h.nrows; r++) out->row_ptr[r] = rs.first[r];
+  c.pos = rs.end;
+  *nnz_out = rs.first[h.nrows];
   *nfull_out = nfull;
   return SLD_OK;
 }

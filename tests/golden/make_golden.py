@@ -369,6 +369,10 @@ def gen_file_cases():
         "bad_zero": frame(M7, 1, 4, [[(1, 2, 14)]]),
         "bad_zero_full": frame(M7, 1, 4, [[(1, 3, 0)]]),
         "bad_col": frame(M7, 1, 4, [[(5, 0, 0)]]),
+        # two errors: the first in file order wins (a zero, then a bad tag)
+        "bad_zero_then_tag": frame(M7, 3, 4, [[(1, 2, 14)], [], [(0, 7, 0)]]),
+        "bad_tag_then_zero": frame(M7, 3, 4, [[(0, 0, 0)], [(1, 9, 0)], [(1, 2, 7)]]),
+        "bad_zero_then_trunc": frame(M7, 5000, 4, [[(1, 0, 0)]] * 4000 + [[(2, 2, 21)]] + [[(0, 0, 0)]] * 999)[:-2],
         "bad_noncanon": frame(M199, 1, 4, [[(1, 3, M199.ell + 2**198)]]),
         "ok_noncanon_small": frame(M200, 1, 4, [[(1, 3, M200.ell + 10)]]),
         "bad_ell": frame(M7, 1, 4, [])[:24] + struct.pack("<H", 1) + bytes([9]) + frame(M7, 1, 4, [])[27:],
