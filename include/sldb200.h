@@ -128,6 +128,10 @@ int sld_vec_create_chains(sld_ctx *ctx, int64_t n, int chains, sld_vec **out);
 int sld_vec_destroy(sld_vec *v);
 int sld_vec_upload_planes(sld_vec *v, const uint64_t *planes, int64_t n, int P);
 int sld_vec_download_planes(sld_vec *v, uint64_t *planes, int64_t n, int P);
+/* The same for a vector of `chains` interleaved chains whose host planes are
+ * separate arrays (planes[g] = chain g, n x P each): no host-side stacking. */
+int sld_vec_upload_planes_chains(sld_vec *v, const uint64_t *const *planes, int64_t n, int P);
+int sld_vec_download_planes_chains(sld_vec *v, uint64_t *const *planes, int64_t n, int P);
 int sld_vec_upload_limbs(sld_vec *v, const uint32_t *limbs, int64_t n);
 int sld_vec_download_limbs(sld_vec *v, uint32_t *limbs, int64_t n);
 /* raw device pointer + stride (words) -- for collectives and tests */

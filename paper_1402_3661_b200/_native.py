@@ -31,6 +31,7 @@ EXPORTS = [
     "sld_mat_create", "sld_mat_create_chains", "sld_mat_destroy", "sld_mat_info",
     "sld_vec_create", "sld_vec_create_chains", "sld_vec_destroy", "sld_vec_upload_planes", "sld_vec_download_planes",
     "sld_vec_upload_limbs", "sld_vec_download_limbs", "sld_vec_device_ptr",
+    "sld_vec_upload_planes_chains", "sld_vec_download_planes_chains",
     "sld_spmv", "sld_spmv_planes", "sld_krylov_unit",
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
     "sld_bench_spmv", "sld_corpus_rows", "sld_corpus_fill",
@@ -90,6 +91,8 @@ def load(build_if_missing=False):
             "sld_vec_upload_planes": ([vp, u64p, i64, i32], i32),
             "sld_vec_download_planes": ([vp, u64p, i64, i32], i32),
             "sld_vec_upload_limbs": ([vp, vp, i64], i32),
+            "sld_vec_upload_planes_chains": ([vp, vp, i64, i32], i32),
+            "sld_vec_download_planes_chains": ([vp, vp, i64, i32], i32),
             "sld_vec_download_limbs": ([vp, vp, i64], i32),
             "sld_vec_device_ptr": ([vp, vp, vp], i32),
             "sld_spmv": ([vp, vp, vp], i32),

@@ -613,7 +613,9 @@ static void host_par(int64_t n, F f) {
 static constexpr int64_t XFER_CHUNK = 1 << 19;  // rows per DMA chunk
 
 // rows of planes (P 16-bit digits in uint64 cells) or limbs (L words) -> device slots
-static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs, int64_t rows, int P) {
+// planes of chain g at planes_g[g] (nullptr: all chains contiguous at `planes`)
+static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs, int64_t rows, int P,
+                       const uint64_t* const* planes_g = nullptr) {
   sld_ctx* c = v->ctx;
   const int L = c->L;
   const int64_t n = rows * v->chains;  // items, chain-major on the host
@@ -627,8 +629,8 @@ static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs
     host_par(hi - lo, [&](int64_t a, int64_t b) {
       for (int64_t r = lo + a; r < lo + b; r++) {
         uint32_t* dst = h + (size_t)r * L;
-        if (planes) {
-          const uint64_t* src = planes + (size_t)r * P;
+        if (planes || planes_g) {
+          const uint64_t* src = planes_g ? planes_g[r / rows] + (size_t)(r % rows) * P : planes + (size_t)r * P;
           for (int j = 0; j < L; j++) {
             const uint32_t d0 = 2 * j < P ? (uint32_t)(src[2 * j] & 0xFFFF) : 0u;
             const uint32_t d1 = 2 * j + 1 < P ? (uint32_t)(src[2 * j + 1] & 0xFFFF) : 0u;
@@ -648,7 +650,8 @@ static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs
   return SLD_OK;
 }
 
-static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t rows, int P) {
+static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t rows, int P,
+                         uint64_t* const* planes_g = nullptr) {
   sld_ctx* c = v->ctx;
   const int L = c->L;
   const int64_t n = rows * v->chains;
@@ -679,8 +682,8 @@ static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t 
     host_par(hi - lo, [&](int64_t a, int64_t b) {
       for (int64_t r = lo + a; r < lo + b; r++) {
         const uint32_t* src = h + (size_t)r * L;
-        if (planes) {
-          uint64_t* dst = planes + (size_t)r * P;
+        if (planes || planes_g) {
+          uint64_t* dst = planes_g ? planes_g[r / rows] + (size_t)(r % rows) * P : planes + (size_t)r * P;
           for (int q = 0; q < P; q++) {
             const int j = q >> 1;
             const uint32_t w = j < L ? src[j] : 0u;
@@ -714,6 +717,24 @@ extern "C" int sld_vec_download_planes(sld_vec* v, uint64_t* planes, int64_t n, 
   TRY(check_P(v->ctx, P));
   CU(cudaSetDevice(v->ctx->dev));
   return download_rows(v, planes, nullptr, n, P);
+}
+
+extern "C" int sld_vec_upload_planes_chains(sld_vec* v, const uint64_t* const* planes, int64_t n, int P) {
+  if (!v || !planes || n != v->n) return fail(SLD_E_ARG, "plane count mismatch");
+  for (int g = 0; g < v->chains; g++)
+    if (!planes[g]) return fail(SLD_E_ARG, "null chain planes");
+  TRY(check_P(v->ctx, P));
+  CU(cudaSetDevice(v->ctx->dev));
+  return upload_rows(v, nullptr, nullptr, n, P, planes);
+}
+
+extern "C" int sld_vec_download_planes_chains(sld_vec* v, uint64_t* const* planes, int64_t n, int P) {
+  if (!v || !planes || n != v->n) return fail(SLD_E_ARG, "plane count mismatch");
+  for (int g = 0; g < v->chains; g++)
+    if (!planes[g]) return fail(SLD_E_ARG, "null chain planes");
+  TRY(check_P(v->ctx, P));
+  CU(cudaSetDevice(v->ctx->dev));
+  return download_rows(v, nullptr, nullptr, n, P, planes);
 }
 
 extern "C" int sld_vec_upload_limbs(sld_vec* v, const uint32_t* limbs, int64_t n) {

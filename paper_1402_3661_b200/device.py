@@ -126,6 +126,21 @@ class DeviceVector:
         N.check(N.load().sld_vec_download_planes(self._h, N.ptr(out), self.n, P))
         return out
 
+    def upload_planes_list(self, planes_list):
+        """One (n, P) planes array per chain, without stacking them on the host."""
+        ps = [np.ascontiguousarray(p, dtype=np.uint64) for p in planes_list]
+        if len(ps) != self.chains or any(p.shape[0] != self.n for p in ps) or \
+                len({p.shape[1] for p in ps}) != 1:
+            raise ValueError("plane count mismatch")
+        ptrs = (ctypes.c_void_p * len(ps))(*[p.ctypes.data for p in ps])
+        N.check(N.load().sld_vec_upload_planes_chains(self._h, ptrs, self.n, ps[0].shape[1]))
+
+    def download_planes_list(self, P):
+        outs = [np.empty((self.n, P), dtype=np.uint64) for _ in range(self.chains)]
+        ptrs = (ctypes.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
+        N.check(N.load().sld_vec_download_planes_chains(self._h, ptrs, self.n, P))
+        return outs
+
     def upload_limbs(self, limbs):
         a = N.cu32(limbs)
         if a.shape != self._shape(self.field.L):

@@ -286,16 +286,16 @@ class B200ChainGroup:
             P = v_planes_list[0].shape[1]
             if self._vec is None:
                 self._vec = dm.vector()
-            self._vec.upload_planes(np.stack(v_planes_list))
+            self._vec.upload_planes_list(v_planes_list)
             terms = dm.krylov_unit(self._vec, xblock.rows, steps)  # (steps, G, m, L)
-            v_out = self._vec.download_planes(P)
+            v_out = self._vec.download_planes_list(P)
         self.count += int(steps)
         m = terms.shape[2]
         out = []
         for g in range(G):
             flat = limbs_to_ints(terms[:, g].reshape(-1, terms.shape[3])) if terms.size else []
             out.append([flat[i * m:(i + 1) * m] for i in range(int(steps))])
-        return out, [v_out[g] for g in range(G)]
+        return out, v_out
 
 
 # the reference's name for the default multiplier
