@@ -148,7 +148,15 @@ struct sld_xblock {
   int m = 0;
   int64_t n = 0;
   uint32_t* x = nullptr;     // [t][j] SW stride: plain (L <= 8, lazy dot products) or Montgomery form
-  uint32_t* fold = nullptr;  // L <= 8: 2^(32k) mod ell for k = L .. 2L (L words each)
+  uint32_t* fold = nullptr;  // L <= 8: 2^(32k) mod ell for k = L .. TC_FOLD_TOP (L words each)
+  // tensor-core projection (L <= 8, m <= 16): X as pre-tiled byte digits
+  int MT = 0;                // 128-row M tiles (0: tensor-core path off)
+  int64_t ktiles = 0;        // 128-byte K tiles (K = n)
+  uint8_t* A = nullptr;      // [ktiles][MT][...] canonical K-major tiles
+  uint8_t* B = nullptr;      // per-step v digits, [ktiles][...]
+  uint32_t* partial = nullptr;
+  int nct = 0;               // CTAs (split K)
+  int64_t kt_per_cta = 0;
 };
 
 struct sld_mat {
@@ -1533,16 +1541,39 @@ extern "C" int sld_xblock_create(sld_ctx* ctx, const uint32_t* x_limbs, int m, i
     if (e != cudaSuccess) return fail(SLD_E_CUDA, "x block upload: %s", cudaGetErrorString(e));
   }
   if (ctx->L <= 8) {
-    // 2^(32k) mod ell, k = L .. 2L, for the lazy dot products' final fold
+    // 2^(32k) mod ell, k = L .. TC_FOLD_TOP, for the final folds of the lazy
+    // and the tensor-core dot products
     const int L = ctx->L;
-    std::vector<uint32_t> r(L, 0), tab((size_t)(L + 1) * L);
+    const int top = std::max(2 * L, TC_FOLD_TOP);
+    std::vector<uint32_t> r(L, 0), tab((size_t)(top - L + 1) * L);
     r[0] = 1;
-    for (int k = 0; k <= 2 * L; k++) {
+    for (int k = 0; k <= top; k++) {
       if (k >= L) std::copy(r.begin(), r.end(), tab.begin() + (size_t)(k - L) * L);
       for (int b = 0; b < 32; b++) hmod_double(r.data(), ctx->mp.ell, L);
     }
     CU(cudaMalloc(&xb->fold, tab.size() * 4));
     CU(cudaMemcpy(xb->fold, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+    // tensor-core path: m <= 16 terms (32 m byte rows <= 4 M tiles).
+    // Measured at cfg3 (tools/bench_dense.py): from m = 4 on it beats the
+    // lazy CUDA-core dot products (m = 16: +0.38 vs +0.73 ms per step); at
+    // m = 2 the lazy path wins (+0.10 vs +0.18 ms).  SLD_DENSE_TC=1 forces it,
+    // =0 disables it.
+    int tc = m >= 4 ? 1 : 0;
+    if (const char* e = getenv("SLD_DENSE_TC")) tc = atoi(e);
+    if (tc && m >= 1 && m <= 16 && n > 0) {
+      xb->MT = (32 * m + 127) / 128;
+      xb->ktiles = (n + TC_BK - 1) / TC_BK;
+      const int64_t max_kt = TC_MAX_K_PER_CTA / TC_BK;
+      xb->nct = (int)std::max<int64_t>(ctx->sms, (xb->ktiles + max_kt - 1) / max_kt);
+      xb->kt_per_cta = (xb->ktiles + xb->nct - 1) / xb->nct;
+      xb->nct = (int)((xb->ktiles + xb->kt_per_cta - 1) / xb->kt_per_cta);
+      CU(cudaMalloc(&xb->A, (size_t)xb->ktiles * xb->MT * TC_MTILE_BYTES));
+      CU(cudaMalloc(&xb->B, (size_t)xb->ktiles * TC_BTILE_BYTES));
+      CU(cudaMalloc(&xb->partial, (size_t)xb->nct * xb->MT * 128 * TC_NQ * 4));
+      ops(L).tc_tile_x(xb->x, m, n, xb->MT, xb->ktiles, xb->A, ctx->stream);
+      CU(cudaGetLastError());
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
   }
   *out = xb.release();
   return SLD_OK;
@@ -1552,6 +1583,9 @@ extern "C" int sld_xblock_destroy(sld_xblock* x) {
   if (!x) return SLD_OK;
   cudaSetDevice(x->ctx->dev);
   if (x->fold) cudaFree(x->fold);
+  if (x->A) cudaFree(x->A);
+  if (x->B) cudaFree(x->B);
+  if (x->partial) cudaFree(x->partial);
   if (x->x) cudaFree(x->x);
   delete x;
   return SLD_OK;
@@ -1588,7 +1622,11 @@ extern "C" int sld_krylov_dense(sld_mat* M, sld_vec* v, sld_xblock* X, int64_t s
     for (int64_t k = 0; k < chunk; k++) {
       da.v = v->buf[v->cur];
       da.out = M->terms_dev + (size_t)k * m * c->SW;
-      if (m) ops(c->L).dense_proj(da, c->mp, c->stream);
+      if (m && X->MT)
+        ops(c->L).tc_project(da.v, v->n, m, X->MT, X->ktiles, X->A, X->B, X->partial, X->nct, X->kt_per_cta,
+                             X->fold, c->mp, da.out, c->stream);
+      else if (m)
+        ops(c->L).dense_proj(da, c->mp, c->stream);
       launch_product(M, v->buf[v->cur], v->buf[v->cur ^ 1], nullptr, 0, nullptr);
       v->cur ^= 1;
     }

@@ -6,6 +6,7 @@
 
 #include "sld_dense.cuh"
 #include "sld_device.cuh"
+#include "sld_tcgemm.cuh"
 
 namespace sld {
 
@@ -29,6 +30,12 @@ struct LOps {
   void (*to_mont)(uint32_t*, int64_t, const ModParams&, cudaStream_t);
   void (*zero_slot)(uint32_t*, cudaStream_t);
   void (*dense_proj)(const DenseProjArgs&, const ModParams&, cudaStream_t);
+  // tensor-core dense projection (L <= 8): tile X once; per step tile v,
+  // digit GEMM, fold.  False when L > 8.
+  bool (*tc_tile_x)(const uint32_t* x, int m, int64_t n, int MT, int64_t ktiles, uint8_t* A, cudaStream_t s);
+  bool (*tc_project)(const uint32_t* v, int64_t n, int m, int MT, int64_t ktiles, const uint8_t* A, uint8_t* B,
+                     uint32_t* partial, int nct, int64_t kt_per_cta, const uint32_t* fold, const ModParams& mp,
+                     uint32_t* out, cudaStream_t s);
   void (*add_mod)(const AddModArgs&, const ModParams&, cudaStream_t);
   void (*read_rows)(const uint32_t*, const int64_t*, int, uint32_t*, cudaStream_t);
   void (*lincomb)(const LinCombArgs&, const ModParams&, cudaStream_t);
@@ -61,6 +68,27 @@ int split_occ() {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_split<L, G, false, false>, 256, 0) != cudaSuccess)
     return 0;
   return n;
+}
+
+template <int MT>
+void launch_tc_gemm_mt(int nct, int64_t ktiles, int64_t kpc, const uint8_t* A, const uint8_t* B, uint32_t* partial,
+                       cudaStream_t s) {
+  static bool attr = [] {
+    cudaFuncSetAttribute(tc_digit_gemm<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(MT));
+    return true;
+  }();
+  (void)attr;
+  tc_digit_gemm<MT><<<nct, TC_THREADS, tc_smem_bytes(MT), s>>>(A, B, ktiles, kpc, partial);
+}
+
+inline void launch_tc_gemm(int MT, int nct, int64_t ktiles, int64_t kpc, const uint8_t* A, const uint8_t* B,
+                           uint32_t* partial, cudaStream_t s) {
+  switch (MT) {
+    case 1: launch_tc_gemm_mt<1>(nct, ktiles, kpc, A, B, partial, s); break;
+    case 2: launch_tc_gemm_mt<2>(nct, ktiles, kpc, A, B, partial, s); break;
+    case 3: launch_tc_gemm_mt<3>(nct, ktiles, kpc, A, B, partial, s); break;
+    default: launch_tc_gemm_mt<4>(nct, ktiles, kpc, A, B, partial, s); break;
+  }
 }
 
 template <int L>
@@ -142,6 +170,24 @@ struct Ops {
   static void dproj(const DenseProjArgs& a, const ModParams& mp, cudaStream_t s) {
     dense_project_launch<L>(a, mp, s);
   }
+  static bool tctx(const uint32_t* x, int m, int64_t n, int MT, int64_t ktiles, uint8_t* A, cudaStream_t s) {
+    if constexpr (L <= 8) {
+      tc_tile_x<L><<<(unsigned)(ktiles * MT), 128, 0, s>>>(x, m, n, MT, ktiles, A);
+      return true;
+    }
+    return false;
+  }
+  static bool tcproj(const uint32_t* v, int64_t n, int m, int MT, int64_t ktiles, const uint8_t* A, uint8_t* B,
+                     uint32_t* partial, int nct, int64_t kt_per_cta, const uint32_t* fold, const ModParams& mp,
+                     uint32_t* out, cudaStream_t s) {
+    if constexpr (L <= 8) {
+      tc_tile_v<L><<<(unsigned)ktiles, 128, 0, s>>>(v, n, ktiles, B);
+      launch_tc_gemm(MT, nct, ktiles, kt_per_cta, A, B, partial, s);
+      tc_proj_final<L><<<m, 1024, 0, s>>>(partial, nct, MT, fold, mp, out);
+      return true;
+    }
+    return false;
+  }
   static void addm(const AddModArgs& a, const ModParams& mp, cudaStream_t s) {
     if (a.n) add_mod_kernel<L><<<blocks_for(a.n, 128), 128, 0, s>>>(a, mp);
   }
@@ -154,7 +200,7 @@ struct Ops {
   static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
     if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);
   }
-  static LOps make() { return LOps{pass, split, split_occupancy, wide, l2s, s2l, mont, zero, dproj, addm, rrows, lcomb, nz}; }
+  static LOps make() { return LOps{pass, split, split_occupancy, wide, l2s, s2l, mont, zero, dproj, tctx, tcproj, addm, rrows, lcomb, nz}; }
 };
 
 template <int L, int LMIN>

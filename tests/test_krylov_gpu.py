@@ -85,17 +85,20 @@ def test_dense_x_vs_oracle():
 
 @pytest.mark.parametrize("bits", [2, 31, 64, 127, 202, 256, 300, 650])
 @pytest.mark.parametrize("extreme", [False, True])
-def test_dense_x_widths_vs_oracle(bits, extreme):
-    # L <= 8: lazy exact dot products (16-bit digit x limb columns, one fold
-    # and Barrett per term); L > 8: Montgomery products.  extreme: x = v =
-    # l - 1 on a longer vector drives every column to its bound
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_dense_x_widths_vs_oracle(bits, extreme, tc, monkeypatch):
+    # L <= 8: tensor-core byte-digit GEMM (tc=1: tcgen05 kind::i8, TMEM) or
+    # lazy exact dot products (tc=0: 16-bit digit x limb columns); one fold
+    # and Barrett per term either way.  L > 8: Montgomery products.
+    # extreme: x = v = l - 1 on a longer vector drives every column to its bound
+    monkeypatch.setenv("SLD_DENSE_TC", tc)
     from paper_1402_3661_b200.modring import next_prime
     ell = 3 if bits == 2 else next_prime((1 << bits) - (1 << (bits // 2)))
     if ell.bit_length() > bits:
         ell = next_prime(1 << (bits - 1))
     mod = PrimeModulus(ell)
     rng = np.random.default_rng(bits + (7 if extreme else 0))
-    n = 3000 if extreme else 200
+    n = 70000 if extreme else 200  # > 512 K tiles of the GEMM: several CTAs
     A = rand_matrix(mod, rng, n, n, 6)
     if extreme:
         y = [ell - 1] * n
