@@ -23,4 +23,9 @@ done
 # one full capture of the dominant kernel (first stripe pass at cfg3)
 timeout 900 ncu --set full --import-source on --graph-profiling node --clock-control none -k regex:spmv_pass -s 8 -c 1 \
   -o $O/full_cfg3_$TAG python tools/profile_spmv.py --config cfg3 --chains 2 --steps 4 > /dev/null 2>&1
+# dense-X projection (tensor-core digit GEMM vs lazy CUDA-core path)
+for tc in 1 0; do SLD_DENSE_TC=$tc timeout 300 python tools/bench_dense.py --config cfg3 --m 2,4,8,16 --steps 48 \
+  > $O/dense_cfg3_tc${tc}_$TAG.txt 2>/dev/null; done
+timeout 600 ncu --set full --graph-profiling node --clock-control none -k regex:tc_digit_gemm -s 2 -c 1 \
+  -o $O/full_tcgemm_$TAG python tools/bench_dense.py --config cfg3 --m 16 --steps 4 > /dev/null 2>&1
 tail -2 $O/gputests_$TAG.log; tail -1 $O/smoke_$TAG.log
