@@ -189,6 +189,8 @@ struct sld_mat {
   uint32_t* part = nullptr;  // slot-indexed partials (npass > 1)
   // limb-sliced passes (one chain, L > 8): T lanes per row, 32 / T rows per slice
   int sliced = 0;
+  // short-row passes (one chain, L <= 8, small N): 4 lanes per row, 8 rows per slice
+  int short_rows = 0;
   // die split (halves == 2): each pass's columns are dealt to the two dies
   int halves = 1;
   int64_t half_chunk = 0;      // columns per interleaved chunk
@@ -927,8 +929,8 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     // 1.36 ms per chain-product), so the split is opt-in.
     int want = 0;
     if (const char* e = getenv("SLD_SPLIT")) want = atoi(e);
-    if (want && !M->sliced && nrows > 0) TRY(ctx_dies(c));
-    if (want && !M->sliced && c->die_n[0] > 0 && c->die_n[1] > 0 && nrows > 0 &&
+    if (want && !M->sliced && !M->short_rows && nrows > 0) TRY(ctx_dies(c));
+    if (want && !M->sliced && !M->short_rows && c->die_n[0] > 0 && c->die_n[1] > 0 && nrows > 0 &&
         ops(L).split_occupancy(M->chains) > 0)
       H = 2;
   }
@@ -1049,7 +1051,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     return tot_s[x] > tot_s[y];
   });
   // rows per slice: one warp holds RH rows x G chains, or RH rows x T limb slices
-  const int RH = M->sliced ? 32 / (SW / 8) : 32 / M->chains;
+  const int RH = M->sliced ? 32 / (SW / 8) : (M->short_rows ? 32 / SHORT_K : 32 / M->chains);
   const int64_t nslices = (nrows + RH - 1) / RH;
   M->nslices = nslices;
   const int64_t nslots = nslices * RH;
@@ -1265,10 +1267,15 @@ extern "C" int sld_mat_create_chains(sld_ctx* ctx, int chains, int64_t nrows, in
   if (const char* pe = getenv("SLD_POLICY")) M->policy = atoi(pe);
   if (const char* pe = getenv("SLD_PF")) M->pf = std::max(0, atoi(pe));
   {
-    // measured: one request per gathered residue instead of SW/8 (cfg5 ...)
+    // wide moduli: one gather request per residue instead of SW/8 (cfg5: 1.15 vs 1.24 ms)
     int wide = 1;
     if (const char* pe = getenv("SLD_WIDE")) wide = atoi(pe);
     M->sliced = (wide && chains == 1 && ctx->SW >= 16) ? 1 : 0;
+    // small matrices: one lane per row leaves most SMs idle (fewer than ~16
+    // warps per SM) and each warp walks its row's groups serially
+    int sh = (chains == 1 && ctx->SW <= 8 && nrows < 32LL * 16 * ctx->sms) ? 1 : 0;
+    if (const char* pe = getenv("SLD_SHORT")) sh = atoi(pe) && chains == 1 && ctx->SW <= 8;
+    M->short_rows = sh;
   }
   if (const char* pe = getenv("SLD_APW")) M->apw = atoi(pe);
   if (const char* pe = getenv("SLD_APW_RATIO")) M->apw_ratio = (float)atof(pe);
@@ -1350,6 +1357,10 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
     a.lane_k4 = M->lane_k4 + (size_t)p * M->nslots;
     if (M->sliced) {
       o.wide(p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
+      continue;
+    }
+    if (M->short_rows) {
+      o.short_pass(p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
       continue;
     }
     if (M->apw && c->apw_max) {

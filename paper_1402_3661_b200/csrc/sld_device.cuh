@@ -314,21 +314,22 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p));
 }
 
-// the +-1 and small entries of one row in one part (column stripe [x half])
-template <int L, int G>
+// the +-1 and small entries of one row in one part (column stripe [x half]);
+// with K lanes per row (short rows) lane `sub` takes groups sub, sub+K, ...
+template <int L, int G, int K = 1>
 __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& si, uint32_t kk, int rw,
                                             const uint32_t* xc, uint64_t pol, uint64_t gpol,
-                                            int64_t (&acc)[L + 1], int64_t& S) {
+                                            int64_t (&acc)[L + 1], int64_t& S, int sub = 0) {
   constexpr int SW = stride_words(L);
   constexpr int NB = spmv_batch<L>();
-  constexpr int R = 32 / G;
+  constexpr int R = 32 / (G * K);
   const uint32_t my_pm = kk & 0xFFFFu, my_s = kk >> 16;
-  const uint32_t PF = a.pf;  // prefetch distance in groups (0: off)
+  const uint32_t PF = a.pf * K;  // prefetch distance in groups (0: off)
   const uint4* pp = a.pm_idx + si.pm_off + rw;
 #pragma unroll 1
-  for (uint32_t k = 0; k < PF && k < my_pm; k++) prefetch_l2(pp + (size_t)k * R);
+  for (uint32_t k = sub; k < PF && k < my_pm; k += K) prefetch_l2(pp + (size_t)k * R);
 #pragma unroll 1
-  for (uint32_t k = 0; k < my_pm; k++) {
+  for (uint32_t k = sub; k < my_pm; k += K) {
     if (PF && k + PF < my_pm) prefetch_l2(pp + (size_t)(k + PF) * R);
     const uint4 w = ld_stream(pp + (size_t)k * R, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
@@ -352,12 +353,12 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
   const uint4* sp = a.s_idx + si.s_off + rw;
   const int4* cp = a.s_coef + si.s_off + rw;
 #pragma unroll 1
-  for (uint32_t k = 0; k < PF && k < my_s; k++) {
+  for (uint32_t k = sub; k < PF && k < my_s; k += K) {
     prefetch_l2(sp + (size_t)k * R);
     prefetch_l2(cp + (size_t)k * R);
   }
 #pragma unroll 1
-  for (uint32_t k = 0; k < my_s; k++) {
+  for (uint32_t k = sub; k < my_s; k += K) {
     if (PF && k + PF < my_s) {
       prefetch_l2(sp + (size_t)(k + PF) * R);
       prefetch_l2(cp + (size_t)(k + PF) * R);
@@ -493,6 +494,55 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
   uint32_t Rr[L];
   finalize<L>(acc, S, mp, Rr);
   store_row<L, G, LAST>(a, slot, chain, Rr, pol);
+}
+
+// ---------------------------------------------------- short-row SpMV pass
+//
+// Small matrices (one chain, L <= 8): a one-lane-per-row warp runs its row's
+// index groups one after another, so a product takes ~groups x (index + gather
+// latency) while most SMs idle.  Here 4 lanes share a row and take every 4th
+// group; their int64 accumulators are summed with shuffles and the row's
+// first lane finishes it.  8 rows per warp, 4x the warps.
+constexpr int SHORT_K = 4;
+
+template <int L, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const SpmvArgs a, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  constexpr int R = 32 / SHORT_K;
+  const int lane = threadIdx.x & 31;
+  const int rw = lane / SHORT_K, sub = lane % SHORT_K;
+  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t slot = slice * R + rw;
+
+  if (FIRST) unit_projection<L, 1>(a);
+  if (slice >= a.nslices) return;
+
+  const uint64_t pol = policy_evict_first();
+  const uint64_t gpol = (a.policy & 1) ? policy_evict_last() : createpolicy_normal();
+  const SliceInfo si = a.slices[slice];
+  const uint32_t kk = a.lane_k4[slot];
+  int64_t acc[L + 1];
+#pragma unroll
+  for (int i = 0; i <= L; i++) acc[i] = 0;
+  int64_t S = 0;
+  row_entries<L, 1, SHORT_K>(a, si, kk, rw, a.x, pol, gpol, acc, S, sub);
+#pragma unroll
+  for (int off = 1; off < SHORT_K; off <<= 1) {
+#pragma unroll
+    for (int i = 0; i <= L; i++) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+    S += __shfl_xor_sync(0xffffffffu, S, off);
+  }
+  if (sub != 0) return;
+  if (!FIRST) {
+    uint32_t pin[SW];
+    load_slot<SW>(a.part_in + (size_t)slot * SW, pin, pol);
+#pragma unroll
+    for (int i = 0; i < L; i++) acc[i] += pin[i];
+  }
+  if (LAST && a.has_full) row_full<L, 1>(a, mp, slot, a.slot_row[slot], a.x, acc);
+  uint32_t Rr[L];
+  finalize<L>(acc, S, mp, Rr);
+  store_row<L, 1, LAST>(a, slot, 0, Rr, pol);
 }
 
 // ------------------------------------------------ limb-sliced SpMV pass

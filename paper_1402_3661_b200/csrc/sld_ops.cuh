@@ -23,6 +23,8 @@ struct LOps {
                 const ModParams& mp);
   // resident CTAs per SM of the die-split kernel for G chains (0: unsupported)
   int (*split_occupancy)(int G);
+  // short-row pass: 4 lanes per row, one chain (false: L > 8)
+  bool (*short_pass)(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a, const ModParams& mp);
   // limb-sliced pass for one chain (false: L <= 8, no slicing)
   bool (*wide)(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a, const ModParams& mp);
   void (*limbs_to_slots)(const uint32_t*, int64_t, uint32_t*, uint32_t, int64_t, int, cudaStream_t);
@@ -142,6 +144,19 @@ struct Ops {
       if (G == 4) return split_occ<L, 4>();
     return 0;
   }
+  static bool shortp(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
+                     const ModParams& mp) {
+    if constexpr (L <= 8) {
+      const unsigned grid = blocks_for(nslices * 32, 256);
+      if (!grid) return true;
+      if (first && last) spmv_short<L, true, true><<<grid, 256, 0, s>>>(a, mp);
+      else if (first) spmv_short<L, true, false><<<grid, 256, 0, s>>>(a, mp);
+      else if (last) spmv_short<L, false, true><<<grid, 256, 0, s>>>(a, mp);
+      else spmv_short<L, false, false><<<grid, 256, 0, s>>>(a, mp);
+      return true;
+    }
+    return false;
+  }
   static bool wide(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
                    const ModParams& mp) {
     if constexpr (wide_T<L>() >= 2) {
@@ -200,7 +215,7 @@ struct Ops {
   static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
     if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);
   }
-  static LOps make() { return LOps{pass, split, split_occupancy, wide, l2s, s2l, mont, zero, dproj, tctx, tcproj, addm, rrows, lcomb, nz}; }
+  static LOps make() { return LOps{pass, split, split_occupancy, shortp, wide, l2s, s2l, mont, zero, dproj, tctx, tcproj, addm, rrows, lcomb, nz}; }
 };
 
 template <int L, int LMIN>

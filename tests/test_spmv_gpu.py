@@ -179,11 +179,12 @@ def test_limb_sliced_vs_oracle(bits, wide):
 
 @pytest.mark.parametrize("chains", [1, 2])
 @pytest.mark.parametrize("stripe", [0, 50])
-def test_die_split_vs_oracle(chains, stripe):
+def test_die_split_vs_oracle(chains, stripe, monkeypatch):
     # SLD_SPLIT=1: columns dealt to the two dies, rows met through the
     # exchange buffer (counters mod 4), several products in a row so the
     # counters and work queues cycle
     from paper_1402_3661_b200 import _native
+    monkeypatch.setenv("SLD_SHORT", "0")  # the split runs on the one-lane-per-row layout
     if _native.die_map(0) is None:
         pytest.skip("die map unavailable on this device")
     rng = np.random.default_rng(11 + chains)
@@ -213,3 +214,25 @@ def test_die_split_vs_oracle(chains, stripe):
     for step in range(3):
         want = [orc.spmv_ints(w) for w in want]
         assert [planes_to_ints(p) for p in outs[step]] == want
+
+
+@pytest.mark.parametrize("short", ["0", "1"])
+@pytest.mark.parametrize("bits", [31, 160, 256])
+def test_short_rows_vs_oracle(short, bits, monkeypatch):
+    # small one-chain matrices: 4 lanes per row (SLD_SHORT=1, shuffled
+    # accumulator sums) or one lane per row; with stripes and dense columns
+    monkeypatch.setenv("SLD_SHORT", short)
+    rng = np.random.default_rng(bits + 3)
+    mod = PrimeModulus(next_prime(1 << (bits - 1)))
+    A = rand_matrix(mod, rng, 500, 499, 45, dense=1, full_frac=0.04, big_small=True)
+    u = mod.random_residues(rng, A.total_cols)
+    want = to_oracle(A).spmv_ints(u)
+    P = digit_count(mod.ell)
+    from paper_1402_3661_b200.modring import planes_to_ints
+    for stripe in (0, 120):
+        dm = DeviceMatrix(A, stripe_cols=stripe)
+        try:
+            assert dm.info()["rows_per_slice"] == (8 if short == "1" else 32)
+            assert planes_to_ints(dm.apply_planes(ints_to_planes(u, P))) == want
+        finally:
+            dm.close()
