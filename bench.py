@@ -52,6 +52,8 @@ DEFAULT_CONFIG = "cfg3"
 # fetched by one instruction of 1-4 lanes (profiles/microbench_r01.txt,
 # microbench2_r01.txt; 96-byte records straddle 128-byte lines)
 L2_GATHER_PEAK_GBS = {1: 9200.0, 2: 15460.0, 3: 12880.0, 4: 16990.0}
+# measured int32 add rate (IADD carry chain, profiles/microbench_r01.txt)
+INT32_PEAK_TOPS = 19.64
 
 
 def dist_env():
@@ -485,6 +487,12 @@ def main():
                             "achieved": gather_bytes / (ms_per_step / 1e3) / 1e9,
                             "frac": gather_bytes / (ms_per_step / 1e3) / 1e9 / gpeak},
         "int_ops_per_product": int_ops(A, L),
+        # SURVEY 8(d)'s IMAD/INT32 side of the roofline: its op count O per
+        # product against the measured int32 add rate (profiles/microbench_r01.txt)
+        "int_roofline": {"bound": "int32", "ops_per_step": G * int_ops(A, L),
+                         "achieved": G * int_ops(A, L) / (ms_per_step / 1e3) / 1e12,
+                         "peak": INT32_PEAK_TOPS, "unit": "Tops/s", "peak_kind": "measured",
+                         "frac": G * int_ops(A, L) / (ms_per_step / 1e3) / 1e12 / INT32_PEAK_TOPS},
         "e2e": {"value": e2e_value, "unit": "SpMV/s", "h2d_bytes_per_step": h2d / e2e_steps,
                 "d2h_bytes_per_step": d2h / e2e_steps, "api": api, "steps": e2e_steps},
         "e2e_apply": {"value": world * G * n_apply / t_apply, "unit": "SpMV/s",
