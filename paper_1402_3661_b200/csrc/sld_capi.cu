@@ -131,6 +131,8 @@ struct sld_ctx {
   void* dstage = nullptr;  // device staging (limb format)
   size_t dstage_bytes = 0;
   size_t apw_max = 0;      // max access-policy window bytes (0: unsupported)
+  uint32_t* fold = nullptr;    // L <= 8: 2^(32k) mod ell, k = L .. TC_FOLD_TOP (lazy folds)
+  uint32_t* coef = nullptr;    // lincomb coefficient staging (64 x SW words)
   uint8_t* die_map = nullptr;  // device copy of the %smid -> die map (256 entries)
   int die_n[2] = {0, 0};       // SMs per die; both 0 if the map is unavailable
 };
@@ -493,6 +495,18 @@ extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pr.persistingL2CacheMaxSize);
   CU(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
+  CU(cudaMalloc(&c->coef, (size_t)64 * c->SW * 4));
+  if (L <= 8) {
+    const int top = std::max(2 * L, TC_FOLD_TOP);
+    std::vector<uint32_t> r(L, 0), tab((size_t)(top - L + 1) * L);
+    r[0] = 1;
+    for (int k = 0; k <= top; k++) {
+      if (k >= L) std::copy(r.begin(), r.end(), tab.begin() + (size_t)(k - L) * L);
+      for (int b = 0; b < 32; b++) hmod_double(r.data(), mp.ell, L);
+    }
+    CU(cudaMalloc(&c->fold, tab.size() * 4));
+    CU(cudaMemcpy(c->fold, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+  }
   *out = c.release();
   return SLD_OK;
 }
@@ -502,6 +516,8 @@ extern "C" int sld_ctx_destroy(sld_ctx* c) {
   cudaSetDevice(c->dev);
   if (c->own) cudaStreamDestroy(c->own);
   if (c->die_map) cudaFree(c->die_map);
+  if (c->fold) cudaFree(c->fold);
+  if (c->coef) cudaFree(c->coef);
   if (c->hstage) cudaFreeHost(c->hstage);
   if (c->dstage) cudaFree(c->dstage);
   delete c;
@@ -766,25 +782,25 @@ extern "C" int sld_lincomb(sld_ctx* c, const uint64_t* y_ptrs, const uint32_t* c
   CU(cudaSetDevice(c->dev));
   LinCombArgs a;
   memset(&a, 0, sizeof(a));
-  uint32_t* dc = nullptr;
   if (k) {
+    // coefficients staged into the context's buffer in stream order (a
+    // previous combination still reading it finishes first); plain for the
+    // lazy L <= 8 kernel, Montgomery form for the CIOS one
     std::vector<uint32_t> h((size_t)k * c->SW, 0);
     for (int j = 0; j < k; j++)
       for (int i = 0; i < c->L; i++) h[(size_t)j * c->SW + i] = coeffs[(size_t)j * c->L + i];
-    CU(cudaMalloc(&dc, h.size() * 4));
-    CU(cudaMemcpyAsync(dc, h.data(), h.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    ops(c->L).to_mont(dc, k, c->mp, c->stream);
+    CU(cudaMemcpyAsync(c->coef, h.data(), h.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    if (c->L > 8) ops(c->L).to_mont(c->coef, k, c->mp, c->stream);
   }
   for (int j = 0; j < k; j++) a.y[j] = (const uint32_t*)(uintptr_t)y_ptrs[j];
-  a.coef = dc;
+  a.coef = c->coef;
+  a.fold = c->fold;
   a.acc = (const uint32_t*)(uintptr_t)acc_ptr;
   a.dst = (uint32_t*)(uintptr_t)dst_ptr;
   a.k = k;
   a.n = n;
   ops(c->L).lincomb(a, c->mp, c->stream);
-  cudaError_t e = cudaStreamSynchronize(c->stream);
-  if (dc) cudaFree(dc);
-  if (e != cudaSuccess) return fail(SLD_E_CUDA, "lincomb: %s", cudaGetErrorString(e));
+  CU(cudaGetLastError());
   return SLD_OK;
 }
 

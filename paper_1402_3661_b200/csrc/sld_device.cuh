@@ -934,12 +934,78 @@ __global__ void add_mod_kernel(const AddModArgs a, const ModParams mp) {
 // product gives c_j y_j mod ell < ell; acc / y_j / dst in biased slots.
 struct LinCombArgs {
   const uint32_t* y[64];
-  const uint32_t* coef;  // k coefficients, SW words each, Montgomery form
+  const uint32_t* coef;  // k coefficients, SW words each: plain (L <= 8, lazy) or Montgomery form
   const uint32_t* acc;   // optional
   uint32_t* dst;
+  const uint32_t* fold;  // L <= 8: 2^(32k) mod ell for k = L .. (L words each)
   int k;
   int64_t n;
 };
+
+// dst = acc + sum_s c_s y_s mod ell for L <= 8, reduced once per element:
+// each 16-bit digit of c_s times each 32-bit limb of y_s[i] (< 2^48) goes into
+// a 64-bit column of weight 2^(16 c) by one IMAD.WIDE (2 L^2 per term, no
+// Montgomery reduction); the columns are carried into 32-bit limbs, the limbs
+// above L folded with 2^(32k) mod ell, and finalize<L> reduces.  k <= 64:
+// every column stays below 64 x L x 2^48 < 2^57.
+template <int L>
+__global__ void __launch_bounds__(256) lincomb_lazy_kernel(const LinCombArgs a, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  constexpr int C = 4 * L - 2;  // columns p + 2j, p < 2L, j < L
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  uint64_t col[C];
+#pragma unroll
+  for (int c = 0; c < C; c++) col[c] = 0;
+  if (a.acc) {
+#pragma unroll
+    for (int j = 0; j < L; j++) col[2 * j] += a.acc[(size_t)i * SW + j] ^ 0x80000000u;
+  }
+  for (int s = 0; s < a.k; s++) {
+    uint32_t u[SW];
+    gather<SW>(a.y[s] + (size_t)i * SW, u);
+    const uint32_t* cw = a.coef + (size_t)s * SW;
+#pragma unroll
+    for (int p = 0; p < 2 * L; p++) {
+      const uint32_t w = __ldg(cw + (p >> 1));
+      const uint32_t d = (p & 1) ? (w >> 16) : (w & 0xFFFFu);
+#pragma unroll
+      for (int j = 0; j < L; j++) col[p + 2 * j] += (uint64_t)d * (u[j] ^ 0x80000000u);
+    }
+  }
+  // 16-bit columns -> 32-bit limbs V[0 .. 2L-2] + the rest `top`
+  constexpr int K = C / 2;
+  uint32_t V[K];
+  uint64_t carry = 0;
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    const uint64_t lo = col[2 * k] + carry;
+    const uint64_t hi = col[2 * k + 1] + (lo >> 16);
+    V[k] = (uint32_t)((lo & 0xFFFFu) | ((hi & 0xFFFFu) << 16));
+    carry = hi >> 16;
+  }
+  int64_t acc[L + 1];
+#pragma unroll
+  for (int j = 0; j < L; j++) acc[j] = V[j];
+  acc[L] = 0;
+#pragma unroll
+  for (int k = L; k <= K + 1; k++) {
+    const uint32_t limb = k < K ? V[k] : (k == K ? (uint32_t)carry : (uint32_t)(carry >> 32));
+    const uint32_t* R = a.fold + (size_t)(k - L) * L;
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+      const uint64_t pr = (uint64_t)limb * __ldg(R + j);
+      acc[j] += (int64_t)(uint32_t)pr;
+      acc[j + 1] += (int64_t)(pr >> 32);
+    }
+  }
+  uint32_t Rr[L];
+  finalize<L>(acc, 0, mp, Rr);
+  uint32_t o[SW];
+#pragma unroll
+  for (int j = 0; j < SW; j++) o[j] = j < L ? (Rr[j] ^ 0x80000000u) : 0u;
+  store_slot<SW>(a.dst + (size_t)i * SW, o);
+}
 
 template <int L>
 __global__ void lincomb_kernel(const LinCombArgs a, const ModParams mp) {

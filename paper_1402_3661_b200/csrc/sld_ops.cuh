@@ -210,7 +210,9 @@ struct Ops {
     if (m) read_rows_kernel<L><<<blocks_for(m, 128), 128, 0, s>>>(v, r, m, o);
   }
   static void lcomb(const LinCombArgs& a, const ModParams& mp, cudaStream_t s) {
-    if (a.n) lincomb_kernel<L><<<blocks_for(a.n, 128), 128, 0, s>>>(a, mp);
+    if (!a.n) return;
+    if constexpr (L <= 8) lincomb_lazy_kernel<L><<<blocks_for(a.n, 256), 256, 0, s>>>(a, mp);
+    else lincomb_kernel<L><<<blocks_for(a.n, 128), 128, 0, s>>>(a, mp);
   }
   static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
     if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);

@@ -10,7 +10,7 @@ from paper_1402_3661_b200 import (
     B200Multiplier, PrimeModulus, SolverFailure, SparseMatrix, mksol_block, mksol_scalar,
     verify_kernel,
 )
-from paper_1402_3661_b200.modring import digit_count, ints_to_planes, planes_to_ints
+from paper_1402_3661_b200.modring import digit_count, ints_to_limbs, ints_to_planes, limbs_to_ints, planes_to_ints
 from paper_1402_3661_b200.solver import _mksol_core
 
 
@@ -81,3 +81,43 @@ def test_mksol_identity_fails_like_reference():
     I = SparseMatrix.from_rows(mod, 4, 4, [[(i, 1)] for i in range(4)])
     with pytest.raises(SolverFailure):
         mksol_scalar(I, [1, 2, 3, 4], [mod.ell - 1, 1])  # X - 1 annihilates I: w = 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [2, 31, 64, 160, 217, 256, 300, 650])
+@pytest.mark.parametrize("k,extreme", [(1, False), (8, False), (64, True), (37, False)])
+def test_lincomb_widths_vs_python(bits, k, extreme):
+    # Mksol's combination dst = acc + sum_j c_j y_j (solver.py:522-536):
+    # lazy 16-bit-digit columns for L <= 8, Montgomery products above;
+    # extreme: every value l - 1 with the maximum k = 64 vectors
+    from paper_1402_3661_b200.device import DeviceVector, Field, lincomb
+    from paper_1402_3661_b200.modring import next_prime
+    ell = 3 if bits == 2 else next_prime((1 << bits) - (1 << (bits // 2)))
+    if ell.bit_length() > bits:
+        ell = next_prime(1 << (bits - 1))
+    mod = PrimeModulus(ell)
+    rng = np.random.default_rng(bits * 100 + k)
+    n = 1000
+    f = Field(mod, 0)
+    if extreme:
+        ys = [[ell - 1] * n for _ in range(k)]
+        cs = [ell - 1] * k
+        acc = [ell - 1] * n
+    else:
+        ys = [mod.random_residues(rng, n) for _ in range(k)]
+        cs = mod.random_residues(rng, k)
+        acc = mod.random_residues(rng, n)
+    dys = []
+    for y in ys:
+        d = DeviceVector(f, n)
+        d.upload_limbs(ints_to_limbs(y, mod.limbs))
+        dys.append(d)
+    da, dst = DeviceVector(f, n), DeviceVector(f, n)
+    da.upload_limbs(ints_to_limbs(acc, mod.limbs))
+    lincomb(f, dys, cs, dst, da)
+    got = limbs_to_ints(dst.download_limbs())
+    want = [(a + sum(c * y[i] for c, y in zip(cs, ys))) % ell for i, a in enumerate(acc)]
+    assert got == want
+    lincomb(f, dys, cs, dst)  # no accumulator
+    assert limbs_to_ints(dst.download_limbs()) == [sum(c * y[i] for c, y in zip(cs, ys)) % ell
+                                                   for i in range(n)]

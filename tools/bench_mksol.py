@@ -1,0 +1,49 @@
+"""Mksol Horner steps on the device (solver.py:508-552): w <- A w + sum_j
+f_j[i] y_j, one SpMV plus one fused combination kernel per step, against the
+plain SpMV step on the same matrix:
+python tools/bench_mksol.py --config cfg3 --n 8 --degree 48"""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1402_3661_b200 import B200Multiplier  # noqa: E402
+from paper_1402_3661_b200.corpus import _random_residue_limbs  # noqa: E402
+from paper_1402_3661_b200.modring import digit_count, limbs_to_planes  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--n", type=int, default=8)
+    ap.add_argument("--degree", type=int, default=48)
+    a = ap.parse_args()
+    cfg = bench.CONFIGS[a.config]
+    A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
+    mul = B200Multiplier(A)
+    rng = np.random.default_rng(4)
+    P = digit_count(mod.ell)
+    Y = [limbs_to_planes(_random_residue_limbs(rng, A.total_cols, mod), P) for _ in range(a.n)]
+    polys = [[int(c) for c in rng.integers(1, 2**62, a.degree + 1)] for _ in range(a.n)]
+    dm = mul.dm
+    v = dm.vector()
+    v.upload_planes(Y[0])
+    dm.bench(v, 4, 0)
+    _, spmv = dm.bench(v, 64, 0)
+    mul.mksol(Y, [p[:3] for p in polys])  # warm-up (allocations)
+    t = time.perf_counter()
+    w, verified, horner, tail = mul.mksol(Y, polys)
+    dt = time.perf_counter() - t
+    print(f"{a.config} mksol n={a.n} degree={a.degree}: {horner} Horner + {tail} tail steps in {dt:.3f} s "
+          f"(incl. upload of {a.n} y blocks) -> {dt / max(1, horner) * 1e3:.3f} ms/step; plain SpMV "
+          f"{spmv:.3f} ms")
+
+
+if __name__ == "__main__":
+    main()
