@@ -35,7 +35,9 @@ CONFIGS = {
     # BASELINE.json configs; bp = (n, m) blocking of the block Wiedemann run
     "cfg1": dict(n=20_000, gamma=20, bits=160, bp=(1, 2), steps=2000, warmup=50, chains=1,
                  desc="configs[0]: synthetic N=20K, gamma=20, 160-bit l (CPU-oracle case)"),
-    "cfg2": dict(n=650_000, gamma=100, bits=217, bp=(1, 2), steps=1000, warmup=20, chains=2,
+    # cfg2 is ONE sequence (bp n = 1), so one chain; chain groups (G = 2, 4)
+    # only apply when block Wiedemann runs n >= 2 sequences (cfg3: n = 8)
+    "cfg2": dict(n=650_000, gamma=100, bits=217, bp=(1, 2), steps=1000, warmup=20, chains=1,
                  desc="configs[1]: GF(2^619)-scale N=650K FFS profile, 217-bit l, one sequence"),
     "cfg3": dict(n=3_600_000, gamma=100, bits=202, bp=(8, 16), steps=400, warmup=10, chains=2,
                  desc="configs[2]: GF(2^809)-scale N=3.6M FFS profile, 202-bit l, "
