@@ -397,6 +397,20 @@ def main():
     value = world * G * steps_even / (total_ms / 1e3)
     launches = steps_even * info["stripes"]
 
+    # the same GPU running ONE sequence (the config's one-chain-per-GPU
+    # deployment), for comparison with the chain-group step above
+    single = None
+    if G > 1:
+        dm1 = DeviceMatrix(A, device=local, chains=1)
+        v1 = dm1.vector()
+        v1.upload_limbs(ys[0])
+        dm1.bench(v1, args.warmup, 0)
+        t1, _ = dm1.bench(v1, args.steps, 0)
+        single = {"value": world * steps_even / (t1 / 1e3), "unit": "SpMV/s",
+                  "ms_per_product": t1 / steps_even, "layout": dm1.info()}
+        v1.close()
+        dm1.close()
+
     # ---- end to end through the public API with host y in, host terms (m
     # per chain and step) and the final iterates out: krylov_column for one
     # chain, the chain group (what krylov_block(chains_per_gpu=G) runs) for G
@@ -477,7 +491,10 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 limbs, exact mod l (int64 lazy accumulation)",
         "data": "synthetic (native corpus generator, FFS profile, seed 1, planted kernel column)",
         "config": dict(config_block(args.config, cfg, A, mod, world), chains_per_gpu=G,
-                       step=f"one product of each of the {G} chain(s) on every GPU"),
+                       step=f"one product of each of the {G} chain(s) on every GPU",
+                       sequences=(f"{G} of the block-Wiedemann sequences per GPU share each matrix pass "
+                                  f"(chain group); one_chain_per_gpu times one sequence per GPU"
+                                  if G > 1 else "one sequence per GPU")),
         "ms_per_chain_product": ms_per_step / G,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -504,6 +521,7 @@ def main():
         "clocks": clk.summary(),
         "clocks_e2e": clk_e2e.summary(),
         "layout": info,
+        "one_chain_per_gpu": single,
         "witness_check": ok_witness,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
