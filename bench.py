@@ -254,7 +254,8 @@ def run_grid(args, cfg, rank, world, local, dist, log):
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
                               RANK="0", WORLD_SIZE="1")
             sk.close()
-        tdist.init_process_group("nccl", timeout=datetime.timedelta(seconds=300))
+        tdist.init_process_group("nccl", timeout=datetime.timedelta(seconds=300),
+                                 device_id=torch.device(f"cuda:{local}"))
     g = GridSpec.parse(args.grid) if args.grid else GridSpec(world, 1)
     A, _, mod = build_matrix(cfg, log)
     t = time.time()
@@ -299,6 +300,8 @@ def run_grid(args, cfg, rank, world, local, dist, log):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if dist is None:  # the private 1-rank group created above
+        tdist.destroy_process_group()
 
 
 def max_over_ranks(dist, x, local):
