@@ -458,6 +458,27 @@ def main():
     for _ in range(n_apply):
         pl = dm.apply_planes(pl)
     t_apply = time.perf_counter() - t0
+    # the reference's OWN krylov_column loop (solver.py:209-214: project,
+    # apply) driving B200Multiplier unchanged: apply() leaves the iterate on
+    # the device, so per step only the m projected rows come back
+    dm_loop = dm if G == 1 else DeviceMatrix(A, device=local, chains=1)
+    mul_loop = B200Multiplier(A, device=local, dm=dm_loop)
+    n_loop = max(min(args.steps, 100), 8)
+    v_loop = y_planes[0]
+    for _ in range(args.warmup):
+        X.project(v_loop)
+        v_loop = mul_loop.apply(v_loop)
+    v_loop = y_planes[0]
+    t0 = time.perf_counter()
+    loop_terms = []
+    for _ in range(n_loop):
+        loop_terms.append(X.project(v_loop))
+        v_loop = mul_loop.apply(v_loop)
+    final_loop = np.asarray(v_loop)
+    t_loop = time.perf_counter() - t0
+    del v_loop, mul_loop
+    if dm_loop is not dm:
+        dm_loop.close()
 
     # ---- kernel correctness spot check at full size: planted witness A w = 0
     ok_witness = None
@@ -519,7 +540,13 @@ def main():
                 "d2h_bytes_per_step": d2h / e2e_steps, "api": api, "steps": e2e_steps},
         "e2e_apply": {"value": world * G * n_apply / t_apply, "unit": "SpMV/s",
                       "h2d_bytes_per_step": G * y_planes[0].nbytes, "d2h_bytes_per_step": G * y_planes[0].nbytes,
-                      "api": "DeviceMatrix.apply_planes (the multiplier's apply) per product"},
+                      "api": "DeviceMatrix.apply_planes: host planes in and out of every product"},
+        "e2e_reference_loop": {"value": world * n_loop / t_loop, "unit": "SpMV/s",
+                               "h2d_bytes_per_step": y_planes[0].nbytes / n_loop,
+                               "d2h_bytes_per_step": (n_loop * bp_m * P * 8 + final_loop.nbytes) / n_loop,
+                               "steps": n_loop,
+                               "api": "the reference's krylov_column loop (project, mul.apply) with "
+                                      "B200Multiplier, one chain: the iterate stays on the device"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "clocks_e2e": clk_e2e.summary(),

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 from . import _native as N
-from .modring import as_modulus, ints_to_limbs
+from .modring import as_modulus, ints_to_limbs, limbs_to_planes
 
 DEFAULT_DEVICE = int(os.environ.get("SLD_DEVICE", "0"))
 
@@ -152,6 +152,14 @@ class DeviceVector:
         N.check(N.load().sld_vec_download_limbs(self._h, N.ptr(out), self.n))
         return out
 
+    def read_rows(self, rows):
+        """Canonical limbs (len(rows), L) of the given rows only (one chain)."""
+        r = N.c64(rows)
+        out = np.empty((len(r), self.field.L), dtype=np.uint32)
+        if len(r):
+            N.check(N.load().sld_vec_read_rows(self._h, N.ptr(r), len(r), N.ptr(out)))
+        return out
+
     def close(self):
         if getattr(self, "_h", None):
             N.load().sld_vec_destroy(self._h)
@@ -171,6 +179,77 @@ def lincomb(field: Field, ys, coeffs, dst: "DeviceVector", acc: "DeviceVector" =
     cl = ints_to_limbs([int(c) for c in coeffs], field.L) if k else np.zeros((0, field.L), np.uint32)
     N.check(N.load().sld_lincomb(field.handle, N.ptr(ptrs), N.ptr(cl), k,
                                  acc.ptr if acc is not None else 0, dst.ptr, dst.n))
+
+
+class DevicePlanes(np.lib.mixins.NDArrayOperatorsMixin):
+    """A product left on the device by `B200Multiplier.apply`.
+
+    It behaves as the (n, P) uint64 digit planes on any host access: numpy
+    functions, operators, attributes. The array is downloaded once and cached
+    read-only. Row indexing (`planes[rows]`, which is what
+    `UnitRows.project` does, solver.py:174-176) fetches only those rows.
+    Passing it back into `apply` keeps the iterate on the device. So the
+    reference's own `krylov_column` (solver.py:199-217), left unmodified,
+    moves m rows per step instead of two full vectors."""
+
+    __array_priority__ = 1000
+
+    def __init__(self, dm: "DeviceMatrix", vec: DeviceVector, P: int):
+        self._dm, self._vec, self._P = dm, vec, int(P)
+        self._host = None
+        self.shape = (vec.n, self._P)
+        self.dtype = np.dtype(np.uint64)
+        self.ndim = 2
+        self.size = vec.n * self._P
+        self.nbytes = self.size * 8
+
+    def __len__(self):
+        return self.shape[0]
+
+    def _materialize(self):
+        if self._host is None:
+            a = self._vec.download_planes(self._P)
+            a.setflags(write=False)
+            self._host = a
+        return self._host
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._materialize()
+        if dtype is not None and np.dtype(dtype) != a.dtype:
+            return a.astype(dtype)
+        return a.copy() if copy else a
+
+    def __array_ufunc__(self, ufunc, method, *inputs, **kwargs):
+        conv = [np.asarray(x) if isinstance(x, DevicePlanes) else x for x in inputs]
+        if "out" in kwargs:
+            kwargs["out"] = tuple(np.asarray(x) if isinstance(x, DevicePlanes) else x for x in kwargs["out"])
+        return getattr(ufunc, method)(*conv, **kwargs)
+
+    def __getitem__(self, idx):
+        if self._host is None and not isinstance(idx, (tuple, slice)):
+            rows = np.asarray(idx)
+            if rows.dtype.kind in "iu" and rows.ndim <= 1:
+                r = np.atleast_1d(rows).astype(np.int64)
+                r = np.where(r < 0, r + self.shape[0], r)
+                if len(r) and (r.min() < 0 or r.max() >= self.shape[0]):
+                    raise IndexError("row index out of range")
+                out = limbs_to_planes(self._vec.read_rows(r), self._P)
+                return out[0] if rows.ndim == 0 else out
+        return self._materialize()[idx]
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self._materialize(), name)
+
+    def __repr__(self):
+        return f"DevicePlanes(shape={self.shape}, on device {self._dm.field.device})"
+
+    def __del__(self):
+        try:
+            self._dm.pool_put(self._vec)
+        except Exception:
+            pass
 
 
 class XBlock:
@@ -240,6 +319,20 @@ class DeviceMatrix:
 
     def vector(self, n=None):
         return DeviceVector(self.field, self.total_cols if n is None else n, self.chains)
+
+    # a few spare iterate buffers, recycled by DevicePlanes (one chain)
+    _POOL_MAX = 4
+
+    def pool_get(self):
+        pool = self.__dict__.setdefault("_pool", [])
+        return pool.pop() if pool else self.vector()
+
+    def pool_put(self, v):
+        pool = self.__dict__.setdefault("_pool", [])
+        if getattr(self, "_h", None) and len(pool) < self._POOL_MAX:
+            pool.append(v)
+        else:
+            v.close()
 
     def apply_planes(self, planes):
         """v = A u on digit planes (host in, host out; chains x n x P when

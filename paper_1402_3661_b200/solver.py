@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .device import DEFAULT_DEVICE, DeviceMatrix, XBlock, lincomb
+from .device import DEFAULT_DEVICE, DeviceMatrix, DevicePlanes, XBlock, lincomb
 from .modring import (
     as_modulus, digit_count, ints_to_limbs, ints_to_planes, limbs_to_ints, limbs_to_planes,
     planes_to_ints, planes_to_limbs,
@@ -109,7 +109,9 @@ class UnitRows:
         self.rows = [int(r) for r in rows]
 
     def project(self, planes) -> list:
-        return planes_to_ints(np.asarray(planes)[self.rows])
+        # row indexing as the reference does (solver.py:174-176): on a
+        # DevicePlanes iterate only these m rows leave the device
+        return planes_to_ints(planes[self.rows])
 
 
 class DenseRows:
@@ -167,10 +169,27 @@ class B200Multiplier:
         return self._dm
 
     def apply(self, planes):
+        """v = A u.  The result stays on the device as `DevicePlanes` (an
+        array on any host access); an iterate that came from this multiplier
+        is not uploaded again, so the reference's per-step loop runs
+        device-resident."""
         with self._lock:
-            out = self.dm.apply_planes(planes)
+            dm = self.dm
+            if isinstance(planes, DevicePlanes) and planes._dm is dm:
+                src, P, own = planes._vec, planes._P, False
+            else:
+                p = np.ascontiguousarray(planes, dtype=np.uint64)
+                if p.ndim != 2 or p.shape[0] != dm.total_cols:
+                    raise ValueError("plane count mismatch")
+                P = p.shape[1]
+                src, own = dm.pool_get(), True
+                src.upload_planes(p)
+            out = dm.pool_get()
+            dm.spmv(src, out)
+            if own:
+                dm.pool_put(src)
         self.count += 1
-        return out
+        return DevicePlanes(dm, out, P)
 
     def krylov(self, xblock, v_planes, steps):
         """`steps` chain steps on the device from iterate `v_planes`:

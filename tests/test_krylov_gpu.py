@@ -251,3 +251,35 @@ def test_native_checkpoint_halt_and_resume(tmp_path):
     assert len(terms) == 19 and terms == full[:19]
     rest, vrest, n = krylov_column(B200Multiplier(A), X, v, 50, start_terms=terms)
     assert n == 31 and rest == full and np.array_equal(vrest, vfull)
+
+
+def test_reference_loop_stays_on_device():
+    # the reference's krylov_column loop body, verbatim in effect
+    # (solver.py:209-214: project, apply, on_step), driven with B200Multiplier:
+    # apply() returns DevicePlanes, the projection reads m rows, and the next
+    # apply() consumes the device iterate -- results equal the oracle
+    from paper_1402_3661_b200.device import DevicePlanes
+    mod = PrimeModulus(2**200 - 75)
+    rng = np.random.default_rng(31)
+    A = rand_matrix(mod, rng, 120, 119, 9, dense=1)
+    y = mod.random_residues(rng, 120)
+    P = digit_count(mod.ell)
+    X = UnitRows([2, 7, 100])
+    mul = B200Multiplier(A)
+    terms, v = [], ints_to_planes(y, P)
+    for _ in range(30):
+        terms.append(X.project(v))
+        v = mul.apply(v)
+        assert isinstance(v, DevicePlanes) and v._host is None  # nothing downloaded
+    orc = to_oracle(A)
+    ot, ov = O.krylov_unit(orc, O.ints_to_limbs(y, mod.limbs), X.rows, 30)
+    assert terms == [O.limbs_to_ints(t) for t in ot]
+    assert planes_to_ints(v) == O.limbs_to_ints(ov)
+    assert mul.count == 30
+    # numpy behaviour on the device iterate
+    host = np.asarray(v)
+    assert host.shape == (120, P) and host.dtype == np.uint64
+    assert np.array_equal(v + 0, host) and bool(np.any(v)) and v.astype("<u2").shape == (120, P)
+    assert np.array_equal(v[[5, 6]], host[[5, 6]]) and np.array_equal(v[3], host[3])
+    with pytest.raises(ValueError):
+        mul.apply(np.zeros((5, P), dtype=np.uint64))
