@@ -558,9 +558,12 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const Sp
 // entries, Barrett finalize, store).  Rows per warp: RH = 32 / T.
 template <int L>
 __host__ __device__ constexpr int wide_T() { return stride_words(L) / 8; }
+#ifndef SLD_WIDE_MINB
+#define SLD_WIDE_MINB 4  // resident CTAs per SM (64 registers; the Barrett tail spills, the gathers don't)
+#endif
 
 template <int L, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(256, 3) spmv_wide(const SpmvArgs a, const ModParams mp) {
+__global__ void __launch_bounds__(256, SLD_WIDE_MINB) spmv_wide(const SpmvArgs a, const ModParams mp) {
   constexpr int SW = stride_words(L);
   constexpr int T = wide_T<L>();
   constexpr int RH = 32 / T;
