@@ -15,7 +15,7 @@ timeout 600 python bench.py --impl reference > $O/bench_ref_cfg3_$TAG.json 2> $O
 timeout 900 ncu --graph-profiling node --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --clock-control none -k regex:spmv_ -c 40 --csv --log-file $O/launches_cfg3_$TAG.csv \
   python bench.py --config cfg3 --steps 4 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-for c in cfg2:2 cfg5:1; do
+for c in cfg2:1 cfg5:1; do
   timeout 600 ncu --graph-profiling node --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none -k regex:spmv_ -c 12 --csv --log-file $O/launches_${c%%:*}_$TAG.csv \
     python tools/profile_spmv.py --config ${c%%:*} --chains ${c##*:} --steps 6 > /dev/null 2>&1
@@ -28,4 +28,8 @@ for tc in 1 0; do SLD_DENSE_TC=$tc timeout 300 python tools/bench_dense.py --con
   > $O/dense_cfg3_tc${tc}_$TAG.txt 2>/dev/null; done
 timeout 600 ncu --set full --graph-profiling node --clock-control none -k regex:tc_digit_gemm -s 2 -c 1 \
   -o $O/full_tcgemm_$TAG python tools/bench_dense.py --config cfg3 --m 16 --steps 4 > /dev/null 2>&1
+# DRAM bytes per step of the benched layouts (bench.py reads profiles/traffic_*.json)
+python tools/traffic_from_launches.py $O/launches_cfg3_$TAG.csv cfg3 2 4 $O/traffic_cfg3_g2_$TAG.json "spmv_pass<7, 2," > /dev/null
+python tools/traffic_from_launches.py $O/launches_cfg2_$TAG.csv cfg2 1 1 $O/traffic_cfg2_g1_$TAG.json > /dev/null
+python tools/traffic_from_launches.py $O/launches_cfg5_$TAG.csv cfg5 1 1 $O/traffic_cfg5_g1_$TAG.json > /dev/null
 tail -2 $O/gputests_$TAG.log; tail -1 $O/smoke_$TAG.log

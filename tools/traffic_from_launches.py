@@ -1,6 +1,6 @@
 """DRAM bytes per step from an ncu launch list (gpu__time_duration.sum,
 dram__bytes_read.sum, dram__bytes_write.sum over the spmv_ kernels):
-python tools/traffic_from_launches.py launches.csv cfg3 G passes_per_step out.json"""
+python tools/traffic_from_launches.py launches.csv cfg3 G passes_per_step out.json [kernel-substring]"""
 import csv
 import io
 import json
@@ -22,6 +22,8 @@ def parse(path):
 def main():
     path, cfg, G, per_step, dst = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), sys.argv[5]
     ls = parse(path)
+    if len(sys.argv) > 6:
+        ls = [x for x in ls if sys.argv[6] in x["kernel"]]
     n = (len(ls) // per_step) * per_step
     last = ls[n - 2 * per_step:n]  # the last two complete steps
     steps = len(last) // per_step
