@@ -290,12 +290,18 @@ __device__ __forceinline__ void finalize(int64_t (&acc)[L + 1], int64_t S, const
 // 128-bit index load of a warp is one coalesced 512-byte transaction.
 // resident CTAs per SM the register allocation must allow: 4 x 256 threads
 // (64 registers) for L <= 8 -- the gathers need every warp they can get
+#ifndef SLD_PASS_MINB
+#define SLD_PASS_MINB 4
+#endif
+#ifndef SLD_PASS_NB
+#define SLD_PASS_NB 4
+#endif
 template <int L>
-__host__ __device__ constexpr int spmv_min_blocks() { return L <= 8 ? 4 : (L <= 16 ? 3 : 2); }
+__host__ __device__ constexpr int spmv_min_blocks() { return L <= 8 ? SLD_PASS_MINB : (L <= 16 ? 3 : 2); }
 // gathers in flight per thread per batch: 4 for one-sector residues, fewer
 // for wide moduli so the accumulator + gathered slots fit the register budget
 template <int L>
-__host__ __device__ constexpr int spmv_batch() { return L <= 8 ? 4 : (L <= 16 ? 2 : 1); }
+__host__ __device__ constexpr int spmv_batch() { return L <= 8 ? SLD_PASS_NB : (L <= 16 ? 2 : 1); }
 
 // G chains share one matrix pass (block Wiedemann's independent sequences):
 // a column's G residues are one contiguous record of G*SW words, and the G
