@@ -283,3 +283,30 @@ def test_reference_loop_stays_on_device():
     assert np.array_equal(v[[5, 6]], host[[5, 6]]) and np.array_equal(v[3], host[3])
     with pytest.raises(ValueError):
         mul.apply(np.zeros((5, P), dtype=np.uint64))
+
+
+@pytest.mark.parametrize("layout", ["split", "pass", "short"])
+def test_krylov_chain_every_layout(layout, monkeypatch):
+    # the device-resident chain (CUDA graphs of 32 products) on each SpMV
+    # kernel family, 70 steps across the graph boundary, against the oracle
+    from paper_1402_3661_b200 import _native
+    env = {"split": {"SLD_SPLIT": "1", "SLD_SHORT": "0"}, "pass": {"SLD_SHORT": "0"},
+           "short": {"SLD_SHORT": "1"}}[layout]
+    if layout == "split" and _native.die_map(0) is None:
+        pytest.skip("die map unavailable")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    mod = PrimeModulus(2**127 - 1)
+    rng = np.random.default_rng(41)
+    A = rand_matrix(mod, rng, 300, 299, 12, dense=1, full_frac=0.03)
+    y = mod.random_residues(rng, 300)
+    rows = [0, 150, 299]
+    P = digit_count(mod.ell)
+    mul = B200Multiplier(A, stripe_cols=100)
+    terms, v, n = krylov_column(mul, UnitRows(rows), ints_to_planes(y, P), 70)
+    orc = to_oracle(A)
+    ot, ov = O.krylov_unit(orc, O.ints_to_limbs(y, mod.limbs), rows, 70)
+    assert n == 70 and terms == [O.limbs_to_ints(t) for t in ot]
+    assert planes_to_ints(v) == O.limbs_to_ints(ov)
+    if layout == "split":
+        assert mul.dm.info()["halves"] == 2

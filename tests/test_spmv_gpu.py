@@ -236,3 +236,46 @@ def test_short_rows_vs_oracle(short, bits, monkeypatch):
             assert planes_to_ints(dm.apply_planes(ints_to_planes(u, P))) == want
         finally:
             dm.close()
+
+
+def _edge_matrices(mod, rng):
+    ell = mod.ell
+    big = mod.random_residues(rng, 1)[0] or 2
+    yield "1x1", SparseMatrix.from_rows(mod, 1, 1, [[(0, ell - 1)]])
+    yield "zero", SparseMatrix.from_rows(mod, 40, 40, [[] for _ in range(40)])
+    yield "one_full", SparseMatrix.from_rows(mod, 3, 3, [[], [(2, big)], []])
+    yield "only_dense", SparseMatrix.from_rows(
+        mod, 33, 31, [[] for _ in range(33)],
+        [(31 + j, mod.random_residues(rng, 33)) for j in range(2)])
+    rows = [[(c, 1) for c in range(0, 37, 2)] if i % 7 == 0 else [] for i in range(37)]
+    yield "ragged", SparseMatrix.from_rows(mod, 37, 37, rows)
+    yield "wide_row", SparseMatrix.from_rows(mod, 2, 3000, [[(c, (c % 5) + 1) for c in range(3000)], []])
+
+
+@pytest.mark.parametrize("bits", [2, 64, 202, 650])
+@pytest.mark.parametrize("layout", ["default", "pass", "split"])
+def test_edge_cases_all_layouts(bits, layout, monkeypatch):
+    # empty / single / ragged / dense-only / full-only / very long rows on
+    # every kernel family: one lane per row, short rows, limb-sliced, die split
+    from paper_1402_3661_b200 import _native
+    if layout == "pass":
+        monkeypatch.setenv("SLD_SHORT", "0")
+        monkeypatch.setenv("SLD_WIDE", "0")
+    if layout == "split":
+        if _native.die_map(0) is None:
+            pytest.skip("die map unavailable")
+        monkeypatch.setenv("SLD_SHORT", "0")
+        monkeypatch.setenv("SLD_SPLIT", "1")
+    mod = PrimeModulus(3 if bits == 2 else next_prime(1 << (bits - 1)))
+    rng = np.random.default_rng(bits)
+    P = digit_count(mod.ell)
+    from paper_1402_3661_b200.modring import planes_to_ints
+    for name, A in _edge_matrices(mod, rng):
+        u = mod.random_residues(rng, A.total_cols)
+        want = to_oracle(A).spmv_ints(u)
+        dm = DeviceMatrix(A)
+        try:
+            got = planes_to_ints(dm.apply_planes(ints_to_planes(u, P)))
+        finally:
+            dm.close()
+        assert got == want, name
