@@ -154,6 +154,15 @@ int sld_add_mod(sld_ctx *ctx, const uint64_t *src_ptrs, int k, uint64_t dst_ptr,
  */
 int sld_lincomb(sld_ctx *ctx, const uint64_t *y_ptrs, const uint32_t *coeffs, int k,
                 uint64_t acc_ptr, uint64_t dst_ptr, int64_t n);
+/* Mksol's combination on the tensor cores (ell < 2^256, n <= 8 vectors):
+ * the y block is tiled once as byte digits; each apply computes
+ * dst = acc + sum_s coeffs[s] y_s mod ell (coeffs n x L limbs; acc may be
+ * 0) as a u8 digit GEMM (tcgen05 kind::i8) with the modular reduction in
+ * the epilogue.  SLD_E_ARG for a modulus of more than 8 limbs or n > 8. */
+typedef struct sld_lcset sld_lcset;
+int sld_lcset_create(sld_ctx *ctx, const uint64_t *y_ptrs, int n, int64_t rows, sld_lcset **out);
+int sld_lcset_apply(sld_lcset *s, const uint32_t *coeffs, uint64_t acc_ptr, uint64_t dst_ptr);
+int sld_lcset_destroy(sld_lcset *s);
 
 /* *out = 1 if any residue of v is non-zero (np.any(planes), solver.py:545). */
 int sld_vec_nonzero(sld_vec *v, int *out);

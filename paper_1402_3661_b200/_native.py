@@ -32,6 +32,7 @@ EXPORTS = [
     "sld_vec_create", "sld_vec_create_chains", "sld_vec_destroy", "sld_vec_upload_planes", "sld_vec_download_planes",
     "sld_vec_upload_limbs", "sld_vec_download_limbs", "sld_vec_device_ptr",
     "sld_vec_upload_planes_chains", "sld_vec_download_planes_chains",
+    "sld_lcset_create", "sld_lcset_apply", "sld_lcset_destroy",
     "sld_spmv", "sld_spmv_planes", "sld_krylov_unit",
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
     "sld_bench_spmv", "sld_corpus_rows", "sld_corpus_fill",
@@ -92,6 +93,9 @@ def load(build_if_missing=False):
             "sld_vec_download_planes": ([vp, u64p, i64, i32], i32),
             "sld_vec_upload_limbs": ([vp, vp, i64], i32),
             "sld_vec_upload_planes_chains": ([vp, vp, i64, i32], i32),
+            "sld_lcset_create": ([vp, vp, i32, i64, pp], i32),
+            "sld_lcset_apply": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64], i32),
+            "sld_lcset_destroy": ([vp], i32),
             "sld_vec_download_planes_chains": ([vp, vp, i64, i32], i32),
             "sld_vec_download_limbs": ([vp, vp, i64], i32),
             "sld_vec_device_ptr": ([vp, vp, vp], i32),

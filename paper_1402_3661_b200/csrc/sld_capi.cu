@@ -804,6 +804,66 @@ extern "C" int sld_lincomb(sld_ctx* c, const uint64_t* y_ptrs, const uint32_t* c
   return SLD_OK;
 }
 
+// ---- Mksol combination on the tensor cores: a fixed set of n <= 8 vectors
+// (the y block) tiled once as byte digits; per Horner step one launch
+// combines them with the step's coefficients and adds acc (sld_tcgemm.cuh)
+struct sld_lcset {
+  sld_ctx* ctx = nullptr;
+  int n = 0;
+  int64_t rows = 0, mtiles = 0;
+  int grid = 0;
+  uint8_t* Y = nullptr;    // [mtiles][n][...] canonical K-major tiles
+};
+
+extern "C" int sld_lcset_create(sld_ctx* c, const uint64_t* y_ptrs, int n, int64_t rows, sld_lcset** out) {
+  if (!c || !out || n < 1 || n > 8 || rows < 0 || !y_ptrs) return fail(SLD_E_ARG, "bad combination set");
+  if (c->L > 8) return fail(SLD_E_ARG, "tensor-core combination needs ell < 2^256");
+  CU(cudaSetDevice(c->dev));
+  auto S = std::make_unique<sld_lcset>();
+  S->ctx = c;
+  S->n = n;
+  S->rows = rows;
+  S->mtiles = (rows + 127) / 128;
+  S->grid = (int)std::max<int64_t>(1, std::min<int64_t>(S->mtiles, c->sms));
+  CU(cudaMalloc(&S->Y, std::max<size_t>((size_t)S->mtiles * tcl_ytile_bytes(n), 16)));
+  uint64_t* dptrs = nullptr;
+  CU(cudaMalloc(&dptrs, 8 * n));
+  CU(cudaMemcpy(dptrs, y_ptrs, 8 * n, cudaMemcpyHostToDevice));
+  if (S->mtiles) ops(c->L).tcl_tile((const uint32_t* const*)dptrs, n, rows, S->mtiles, S->Y, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaFree(dptrs);
+  if (e != cudaSuccess) return fail(SLD_E_CUDA, "combination set: %s", cudaGetErrorString(e));
+  *out = S.release();
+  return SLD_OK;
+}
+
+extern "C" int sld_lcset_destroy(sld_lcset* S) {
+  if (!S) return SLD_OK;
+  cudaSetDevice(S->ctx->dev);
+  cudaStreamSynchronize(S->ctx->stream);
+  if (S->Y) cudaFree(S->Y);
+  delete S;
+  return SLD_OK;
+}
+
+// dst = acc + sum_s coeffs[s] y_s mod ell (coeffs: n x L limbs, canonical;
+// acc may be 0).  Asynchronous on the context stream.
+extern "C" int sld_lcset_apply(sld_lcset* S, const uint32_t* coeffs, uint64_t acc_ptr, uint64_t dst_ptr) {
+  if (!S || !coeffs || !dst_ptr) return fail(SLD_E_ARG, "bad combination arguments");
+  sld_ctx* c = S->ctx;
+  CU(cudaSetDevice(c->dev));
+  const int L = c->L;
+  TclCoef cf;
+  memset(&cf, 0, sizeof(cf));
+  for (int s = 0; s < S->n; s++)
+    for (int i = 0; i < L; i++) cf.w[s][i] = coeffs[(size_t)s * L + i];
+  if (S->mtiles)
+    ops(L).tcl_apply(S->Y, cf, S->n, S->rows, S->mtiles, S->grid, (const uint32_t*)(uintptr_t)acc_ptr,
+                     (uint32_t*)(uintptr_t)dst_ptr, c->fold, c->mp, c->stream);
+  CU(cudaGetLastError());
+  return SLD_OK;
+}
+
 extern "C" int sld_vec_nonzero(sld_vec* v, int* out) {
   if (!v || !out) return fail(SLD_E_ARG, "null argument");
   sld_ctx* c = v->ctx;

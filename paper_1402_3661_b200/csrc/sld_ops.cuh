@@ -35,6 +35,10 @@ struct LOps {
   // tensor-core dense projection (L <= 8): tile X once; per step tile v,
   // digit GEMM, fold.  False when L > 8.
   bool (*tc_tile_x)(const uint32_t* x, int m, int64_t n, int MT, int64_t ktiles, uint8_t* A, cudaStream_t s);
+  // tensor-core Mksol combination (L <= 8, n <= 8): tile the y set once, combine per step
+  bool (*tcl_tile)(const uint32_t* const* ys_dev, int n, int64_t rows, int64_t mtiles, uint8_t* Y, cudaStream_t s);
+  bool (*tcl_apply)(const uint8_t* Y, const TclCoef& cf, int n, int64_t rows, int64_t mtiles, int grid,
+                    const uint32_t* acc, uint32_t* dst, const uint32_t* fold, const ModParams& mp, cudaStream_t s);
   bool (*tc_project)(const uint32_t* v, int64_t n, int m, int MT, int64_t ktiles, const uint8_t* A, uint8_t* B,
                      uint32_t* partial, int nct, int64_t kt_per_cta, const uint32_t* fold, const ModParams& mp,
                      uint32_t* out, cudaStream_t s);
@@ -192,6 +196,28 @@ struct Ops {
     }
     return false;
   }
+  static bool tcltile(const uint32_t* const* ys, int n, int64_t rows, int64_t mtiles, uint8_t* Y, cudaStream_t s) {
+    if constexpr (L <= 8) {
+      const int64_t cores = mtiles * n * 32;
+      tcl_tile_y<L><<<blocks_for(cores, 128), 128, 0, s>>>(ys, n, rows, mtiles, Y);
+      return true;
+    }
+    return false;
+  }
+  static bool tclapply(const uint8_t* Y, const TclCoef& cf, int n, int64_t rows, int64_t mtiles, int grid,
+                       const uint32_t* acc, uint32_t* dst, const uint32_t* fold, const ModParams& mp,
+                       cudaStream_t s) {
+    if constexpr (L <= 8) {
+      static bool attr = [] {
+        cudaFuncSetAttribute(tcl_combine<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl_smem_bytes(8));
+        return true;
+      }();
+      (void)attr;
+      tcl_combine<L><<<grid, TCL_THREADS, tcl_smem_bytes(n), s>>>(Y, cf, n, rows, mtiles, acc, dst, fold, mp);
+      return true;
+    }
+    return false;
+  }
   static bool tcproj(const uint32_t* v, int64_t n, int m, int MT, int64_t ktiles, const uint8_t* A, uint8_t* B,
                      uint32_t* partial, int nct, int64_t kt_per_cta, const uint32_t* fold, const ModParams& mp,
                      uint32_t* out, cudaStream_t s) {
@@ -217,7 +243,7 @@ struct Ops {
   static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
     if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);
   }
-  static LOps make() { return LOps{pass, split, split_occupancy, shortp, wide, l2s, s2l, mont, zero, dproj, tctx, tcproj, addm, rrows, lcomb, nz}; }
+  static LOps make() { return LOps{pass, split, split_occupancy, shortp, wide, l2s, s2l, mont, zero, dproj, tctx, tcltile, tclapply, tcproj, addm, rrows, lcomb, nz}; }
 };
 
 template <int L, int LMIN>

@@ -45,6 +45,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
                  : "r"(smem_u32(b)), "r"(parity)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
@@ -311,6 +314,219 @@ __global__ void __launch_bounds__(1024) tc_proj_final(const uint32_t* __restrict
   finalize<L>(acc, 0, mp, Rr);
 #pragma unroll
   for (int i = 0; i < SW; i++) out[(size_t)t * SW + i] = i < L ? Rr[i] : 0u;
+}
+
+// ------------------------------------------------------------------------
+// Mksol's combination on the tensor cores (solver.py:522-536):
+//     w[i] = acc[i] + sum_s c_s y_s[i]  mod ell,  s < n <= 8.
+// With bytes y_s[i] = sum_q Y_{s,q} 2^(8q) and c_s = sum_p C_{s,p} 2^(8p):
+//     sum_s c_s y_s[i] = sum_k 2^(8k) D[i][k],
+//     D = Y' . C'^T,  Y'[i][(s,q)] = Y_{s,q}[i],  C'[k][(s,q)] = C_{s,k-q}.
+// M = rows i (128 per tile), N = 64 byte positions k, K = 32 n.  Every D
+// entry is < 256 * 255^2 < 2^24.  The epilogue reads its row's 64 columns
+// from TMEM, carries them into limbs, folds the limbs above L with
+// 2^(32k) mod ell, adds acc, and runs finalize: w is written once, never
+// staged.  Y' (the n fixed vectors) is tiled once per Mksol run; C'
+// (n x 2 KB) is expanded in shared memory from the step's coefficients.
+constexpr int TCL_N = 64;                       // byte positions k of the products
+constexpr uint32_t TCL_IDESC = (2u << 4) | ((uint32_t)(TCL_N >> 3) << 17) | ((128u >> 4) << 24);
+constexpr int TCL_STAGES = 3;
+constexpr int TCL_THREADS = 192;
+
+__host__ __device__ constexpr int tcl_ytile_bytes(int n) { return 128 * 32 * n; }
+__host__ __device__ constexpr int tcl_b_bytes(int n) { return TCL_N * 32 * n; }
+__host__ __device__ constexpr int tcl_smem_bytes(int n) {
+  return TCL_STAGES * tcl_ytile_bytes(n) + tcl_b_bytes(n) + 1024;
+}
+
+// y_s (biased slots) -> Y' tiles: tile mt = [s][mg][kc][8 rows][16 bytes];
+// one thread per 128-byte core matrix (the 16 bytes of a row are 4 limb words)
+template <int L>
+__global__ void tcl_tile_y(const uint32_t* const* __restrict__ ys, int n, int64_t rows, int64_t mtiles,
+                           uint8_t* __restrict__ Y) {
+  constexpr int SW = stride_words(L);
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per_tile = (int64_t)n * 32;
+  if (idx >= mtiles * per_tile) return;
+  const int64_t mt = idx / per_tile;
+  const int c = (int)(idx % per_tile);
+  const int s = c >> 5, mg = (c >> 1) & 15, kc = c & 1;
+  uint32_t o[32];
+#pragma unroll
+  for (int rr = 0; rr < 8; rr++) {
+    const int64_t i = mt * 128 + mg * 8 + rr;
+#pragma unroll
+    for (int w = 0; w < 4; w++) {
+      const int limb = kc * 4 + w;
+      o[rr * 4 + w] = (i < rows && limb < L) ? (ys[s][(size_t)i * SW + limb] ^ 0x80000000u) : 0u;
+    }
+  }
+  uint4* dst = reinterpret_cast<uint4*>(Y + (size_t)idx * 128);
+#pragma unroll
+  for (int q = 0; q < 8; q++) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+}
+
+// the step's coefficients travel as kernel parameters (n x 8 words) and
+// every CTA expands them into its C' tiles in shared memory: no copy, no
+// host synchronisation between Horner steps
+struct TclCoef {
+  uint32_t w[8][8];  // [s][limb], canonical
+};
+
+template <int L>
+__global__ void __launch_bounds__(TCL_THREADS, 1)
+    tcl_combine(const uint8_t* __restrict__ Y, const TclCoef cf, int n, int64_t rows,
+                int64_t mtiles, const uint32_t* __restrict__ acc, uint32_t* __restrict__ dst,
+                const uint32_t* __restrict__ fold, const ModParams mp) {
+  constexpr int SW = stride_words(L);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t YT = tcl_ytile_bytes(n), BB = tcl_b_bytes(n);
+  uint8_t* sB = smem + TCL_STAGES * YT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + BB);
+  uint64_t* empty = full + TCL_STAGES;
+  uint64_t* tfull = empty + TCL_STAGES;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // this CTA's tiles: mt = blockIdx.x + j gridDim.x
+  const int64_t ntile = blockIdx.x < mtiles ? (mtiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TCL_STAGES; s++) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  // C'[k][(s, q)] = byte (k - q) of c_s, tiled [s][mg][kc][8 rows][16 bytes]:
+  // word w of the tile holds 4 consecutive q of one (s, k)
+  for (int w = threadIdx.x; w < (int)(BB / 4); w += blockDim.x) {
+    const int byte0 = w * 4;
+    const int s_ = byte0 / (TCL_N * 32), rem = byte0 % (TCL_N * 32);
+    const int mg = rem >> 8, kc = (rem >> 7) & 1, rr = (rem >> 4) & 7, jj0 = rem & 15;
+    const int k = mg * 8 + rr;
+    uint32_t word = 0;
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const int p = k - (kc * 16 + jj0 + b);
+      const uint32_t v = (p >= 0 && p < 32) ? (cf.w[s_][p >> 2] >> (8 * (p & 3))) & 0xFFu : 0u;
+      word |= v << (8 * b);
+    }
+    reinterpret_cast<uint32_t*>(sB)[w] = word;
+  }
+  // generic-proxy shared stores -> visible to the tensor core (async proxy)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    for (int64_t j = 0; j < ntile; j++) {
+      const int s = (int)(j % TCL_STAGES);
+      if (j >= TCL_STAGES) mbar_wait(empty + s, (uint32_t)((j / TCL_STAGES - 1) & 1));
+      mbar_expect_tx(full + s, YT);
+      bulk_g2s(smem + s * YT, Y + (size_t)(blockIdx.x + j * gridDim.x) * YT, YT, full + s);
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int64_t j = 0; j < ntile; j++) {
+      const int s = (int)(j % TCL_STAGES);
+      const int b = (int)(j & 1);
+      mbar_wait(full + s, (uint32_t)((j / TCL_STAGES) & 1));
+      if (j >= 2) mbar_wait(tempty + b, (uint32_t)((j / 2 - 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint8_t* sy = smem + s * YT;
+      for (int ks = 0; ks < n; ks++) {
+        const uint64_t ad = umma_desc(sy + ks * (128 * 32));
+        const uint64_t bd = umma_desc(sB + ks * (TCL_N * 32));
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (uint32_t)(b * TCL_N)),
+            "l"(ad), "l"(bd), "r"(TCL_IDESC), "r"(ks > 0 ? 1u : 0u));
+      }
+      umma_commit(empty + s);
+      umma_commit(tfull + b);
+    }
+  } else if (warp >= 2) {
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    for (int64_t j = 0; j < ntile; j++) {
+      const int b = (int)(j & 1);
+      mbar_wait(tfull + b, (uint32_t)((j / 2) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t d[TCL_N];
+      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * TCL_N);
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(d[32 * h + 0]), "=r"(d[32 * h + 1]), "=r"(d[32 * h + 2]), "=r"(d[32 * h + 3]),
+              "=r"(d[32 * h + 4]), "=r"(d[32 * h + 5]), "=r"(d[32 * h + 6]), "=r"(d[32 * h + 7]),
+              "=r"(d[32 * h + 8]), "=r"(d[32 * h + 9]), "=r"(d[32 * h + 10]), "=r"(d[32 * h + 11]),
+              "=r"(d[32 * h + 12]), "=r"(d[32 * h + 13]), "=r"(d[32 * h + 14]), "=r"(d[32 * h + 15]),
+              "=r"(d[32 * h + 16]), "=r"(d[32 * h + 17]), "=r"(d[32 * h + 18]), "=r"(d[32 * h + 19]),
+              "=r"(d[32 * h + 20]), "=r"(d[32 * h + 21]), "=r"(d[32 * h + 22]), "=r"(d[32 * h + 23]),
+              "=r"(d[32 * h + 24]), "=r"(d[32 * h + 25]), "=r"(d[32 * h + 26]), "=r"(d[32 * h + 27]),
+              "=r"(d[32 * h + 28]), "=r"(d[32 * h + 29]), "=r"(d[32 * h + 30]), "=r"(d[32 * h + 31])
+            : "r"(ta + (uint32_t)(32 * h)));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(tempty + b);
+      const int64_t i = (int64_t)(blockIdx.x + j * gridDim.x) * 128 + row;
+      if (i >= rows) continue;
+      // bytes (weights 2^(8k)) -> 32-bit limbs V[0..16]
+      uint32_t V[17];
+      uint64_t carry = 0;
+#pragma unroll
+      for (int w = 0; w < 16; w++) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int bb = 0; bb < 4; bb++) {
+          const uint64_t t = carry + d[4 * w + bb];
+          word |= (uint32_t)(t & 0xFF) << (8 * bb);
+          carry = t >> 8;
+        }
+        V[w] = word;
+      }
+      V[16] = (uint32_t)carry;  // < 2^25
+      int64_t a2[L + 1];
+#pragma unroll
+      for (int q = 0; q < L; q++) a2[q] = (int64_t)V[q] + (acc ? (int64_t)(acc[(size_t)i * SW + q] ^ 0x80000000u) : 0);
+      a2[L] = 0;
+#pragma unroll
+      for (int k = L; k < 17; k++) {
+        const uint32_t* R = fold + (size_t)(k - L) * L;
+#pragma unroll
+        for (int q = 0; q < L; q++) {
+          const uint64_t pr = (uint64_t)V[k] * __ldg(R + q);
+          a2[q] += (int64_t)(uint32_t)pr;
+          a2[q + 1] += (int64_t)(pr >> 32);
+        }
+      }
+      uint32_t Rr[L];
+      finalize<L>(a2, 0, mp, Rr);
+      uint32_t o[SW];
+#pragma unroll
+      for (int q = 0; q < SW; q++) o[q] = q < L ? (Rr[q] ^ 0x80000000u) : 0u;
+      store_slot<SW>(dst + (size_t)i * SW, o);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+  }
 }
 
 }  // namespace sld

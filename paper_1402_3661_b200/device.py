@@ -181,6 +181,34 @@ def lincomb(field: Field, ys, coeffs, dst: "DeviceVector", acc: "DeviceVector" =
                                  acc.ptr if acc is not None else 0, dst.ptr, dst.n))
 
 
+class LinCombSet:
+    """n <= 8 fixed device vectors combined on the tensor cores (Mksol's
+    Horner combination, sld_lcset_*): dst = acc + sum_s c_s y_s mod l."""
+
+    def __init__(self, field: Field, ys, rows: int):
+        self.field, self.n = field, len(ys)
+        ptrs = np.array([y.ptr for y in ys], dtype=np.uint64)
+        h = ctypes.c_void_p()
+        N.check(N.load().sld_lcset_create(field.handle, N.ptr(ptrs), self.n, int(rows), ctypes.byref(h)))
+        self._h = h
+        self._ys = list(ys)  # keep the vectors alive while tiled copies are in use
+
+    def apply(self, coeffs, dst: "DeviceVector", acc: "DeviceVector" = None):
+        cl = ints_to_limbs([int(c) for c in coeffs], self.field.L)
+        N.check(N.load().sld_lcset_apply(self._h, N.ptr(cl), acc.ptr if acc is not None else 0, dst.ptr))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.load().sld_lcset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DevicePlanes(np.lib.mixins.NDArrayOperatorsMixin):
     """A product left on the device by `B200Multiplier.apply`.
 

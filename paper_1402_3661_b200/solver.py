@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .device import DEFAULT_DEVICE, DeviceMatrix, DevicePlanes, XBlock, lincomb
+from .device import DEFAULT_DEVICE, DeviceMatrix, DevicePlanes, LinCombSet, XBlock, lincomb
 from .modring import (
     as_modulus, digit_count, ints_to_limbs, ints_to_planes, limbs_to_ints, limbs_to_planes,
     planes_to_ints, planes_to_limbs,
@@ -235,8 +235,16 @@ class B200Multiplier:
                 y.upload_planes(yp)
                 ys.append(y)
             w, t = dm.vector(), dm.vector()
+            # tensor-core combination (l < 2^256, n <= 8 y vectors), else
+            # the lazy CUDA-core kernel
+            lc = None
+            if dm.L <= 8 and 1 <= len(ys) <= 8 and os.environ.get("SLD_MKSOL_TC", "1") != "0":
+                lc = LinCombSet(dm.field, ys, dm.total_cols)
 
             def combo(i, acc, dst):
+                if lc is not None:
+                    lc.apply([p[i] if i <= _poly_degree(p) else 0 for p in G], dst, acc)
+                    return
                 sel = [(ys[j], p[i]) for j, p in enumerate(G) if i <= _poly_degree(p) and p[i]]
                 for k0 in range(0, max(1, len(sel)), 64):
                     part = sel[k0:k0 + 64]
@@ -258,6 +266,8 @@ class B200Multiplier:
             verified = (not t.nonzero()) and w.nonzero()
             w_nonzero = w.nonzero()
             w_planes = w.download_planes(P)
+            if lc is not None:
+                lc.close()
             for v in ys + [w, t]:
                 v.close()
         self.count += horner + tail + 1

@@ -121,3 +121,45 @@ def test_lincomb_widths_vs_python(bits, k, extreme):
     lincomb(f, dys, cs, dst)  # no accumulator
     assert limbs_to_ints(dst.download_limbs()) == [sum(c * y[i] for c, y in zip(cs, ys)) % ell
                                                    for i in range(n)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [2, 31, 64, 160, 217, 256])
+@pytest.mark.parametrize("n,extreme", [(1, False), (3, False), (8, False), (8, True)])
+def test_tensor_core_combination_vs_python(bits, n, extreme):
+    # sld_lcset: dst = acc + sum_s c_s y_s as a u8 digit GEMM (tcgen05
+    # kind::i8) with the mod-l reduction in the epilogue; rows spanning
+    # several 128-row tiles and a ragged last tile; zero coefficients
+    from paper_1402_3661_b200.device import DeviceVector, Field, LinCombSet
+    from paper_1402_3661_b200.modring import next_prime
+    ell = 3 if bits == 2 else next_prime((1 << bits) - (1 << (bits // 2)))
+    if ell.bit_length() > bits:
+        ell = next_prime(1 << (bits - 1))
+    mod = PrimeModulus(ell)
+    rng = np.random.default_rng(bits * 10 + n)
+    rows = 20000 + 77
+    f = Field(mod, 0)
+    if extreme:
+        ys = [[ell - 1] * rows for _ in range(n)]
+        acc = [ell - 1] * rows
+    else:
+        ys = [mod.random_residues(rng, rows) for _ in range(n)]
+        acc = mod.random_residues(rng, rows)
+    dys = []
+    for y in ys:
+        d = DeviceVector(f, rows)
+        d.upload_limbs(ints_to_limbs(y, mod.limbs))
+        dys.append(d)
+    da, dst = DeviceVector(f, rows), DeviceVector(f, rows)
+    da.upload_limbs(ints_to_limbs(acc, mod.limbs))
+    lc = LinCombSet(f, dys, rows)
+    for trial in range(3):
+        cs = [ell - 1] * n if extreme else mod.random_residues(rng, n)
+        if trial == 2 and n > 1:
+            cs[0] = 0
+        lc.apply(cs, dst, da if trial != 1 else None)
+        got = limbs_to_ints(dst.download_limbs())
+        base = acc if trial != 1 else [0] * rows
+        want = [(a + sum(c * y[i] for c, y in zip(cs, ys))) % ell for i, a in enumerate(base)]
+        assert got == want, trial
+    lc.close()
