@@ -260,8 +260,24 @@ def run_grid(args, cfg, rank, world, local, dist, log):
     A, _, mod = build_matrix(cfg, log)
     t = time.time()
     perm = balance_permutation(A, g)
-    grid = B200Grid(A, g, GridComm(g), device=local, perm=perm)
-    log(f"grid {g} node {(grid.i, grid.j)} block built in {time.time() - t:.1f}s")
+    fused = g.c == 1 and args.grid_impl == "peer"
+    if fused:
+        # r x 1: the all-gather fused into the SpMV epilogue (peer stores +
+        # flag barrier, paper_1402_3661_b200/peergrid.py)
+        from paper_1402_3661_b200 import _native as N
+        from paper_1402_3661_b200.peergrid import PeerRowGrid
+        torch.cuda.set_device(local)
+
+        def exchange(obj):
+            out = [None] * world
+            tdist.all_gather_object(out, obj)
+            return out
+        grid = PeerRowGrid(A, g.r, rank, exchange, device=local, perm=perm)
+        N.check(N.load().sld_ctx_set_stream(grid.field.handle, torch.cuda.current_stream(local).cuda_stream))
+        log(f"peer-push grid {g} node {rank} block built in {time.time() - t:.1f}s")
+    else:
+        grid = B200Grid(A, g, GridComm(g), device=local, perm=perm)
+        log(f"grid {g} node {(grid.i, grid.j)} block built in {time.time() - t:.1f}s")
     y = _random_residue_limbs(np.random.default_rng(3), grid.n_padded, mod)
     grid.load_vector(y)
     grid.iterate(args.warmup)
@@ -278,7 +294,20 @@ def run_grid(args, cfg, rank, world, local, dist, log):
     t_all = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
     tdist.all_reduce(t_all, op=tdist.ReduceOp.MAX)
     ms = float(t_all.item())
-    last = grid.comm_log.entries[-1]
+    if fused:
+        W = 4 * mod.limbs
+        comm = {"impl": "SpMV epilogue peer stores + flag barrier (no collective)",
+                "bytes_per_iter_reference_accounting": (g.r - 1) * grid.n_padded * mod.byte_width,
+                "wire_bytes_per_iter": (g.r - 1) * grid.n_padded * 32 * ((W + 31) // 32),
+                "messages_per_iter": 0}
+        stripes = grid.dm.info()["stripes"]
+    else:
+        last = grid.comm_log.entries[-1]
+        comm = {"impl": "NCCL p2p (collector reduce + broadcast, gridmv.py:251-348)",
+                "bytes_per_iter_reference_accounting": last.total_bytes,
+                "wire_bytes_per_iter": last.reduce.wire_bytes + last.broadcast.wire_bytes,
+                "messages_per_iter": last.reduce.messages + last.broadcast.messages}
+        stripes = grid.engine.dm.info()["stripes"]
     B, Z, Zs, Zf = algorithmic_bytes(A, mod.limbs)
     peak, peak_kind = measured_peaks()
     per = ms / args.steps
@@ -288,18 +317,20 @@ def run_grid(args, cfg, rank, world, local, dist, log):
         "scaling": "strong", "vs_baseline": None, "dtype": "u32 limbs, exact mod l",
         "data": "synthetic (native corpus generator, FFS profile, seed 1)",
         "config": dict(config_block("cfg4", cfg, A, mod, world), grid=str(g),
-                       parallelism=f"one chain on a {g} grid (NCCL p2p / all-gather)"),
+                       parallelism=(f"one chain on a {g} grid, all-gather fused into the SpMV (peer stores)"
+                                    if fused else f"one chain on a {g} grid (NCCL p2p / all-gather)")),
         "roofline": {"bound": "hbm", "achieved": B / world / (per / 1e3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": B / world / (per / 1e3) / 1e9 / peak, "traffic": None,
                      "peak_kind": peak_kind},
-        "comm": {"bytes_per_iter_reference_accounting": last.total_bytes,
-                 "wire_bytes_per_iter": last.reduce.wire_bytes + last.broadcast.wire_bytes,
-                 "messages_per_iter": last.reduce.messages + last.broadcast.messages},
-        "gpu_launches": args.steps * (grid.engine.dm.info()["stripes"] + (1 if g.c > 1 else 0)),
+        "comm": comm,
+        "gpu_launches": args.steps * (stripes + (1 if (g.c > 1 or fused) else 0)),
         "clocks": clk.summary(),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if fused:
+        tdist.barrier()  # no peer may still push into buffers about to be freed
+        grid.close()
     if dist is None:  # the private 1-rank group created above
         tdist.destroy_process_group()
 
@@ -330,6 +361,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--grid", default=None, help="cfg4 grid RxC (default: <gpus>x1)")
+    ap.add_argument("--grid-impl", default="peer", choices=["peer", "nccl"],
+                    help="cfg4 r x 1 exchange: fused peer stores (default) or the NCCL node protocol")
     ap.add_argument("--chains", type=int, default=None,
                     help="Krylov chains advanced per matrix pass on each GPU (1, 2, 4)")
     args = ap.parse_args()

@@ -259,6 +259,23 @@ int sld_sldv_write(const char *path, int kind, const uint32_t *ell, int L, int64
 int sld_sldv_info(const char *path, int header_only, int64_t *info, uint8_t *ell_be, int ell_cap);
 int sld_sldv_read(const char *path, uint32_t *limbs, int stride);
 
+/*
+ * r x 1 grid with the all-gather fused into the SpMV (the
+ * fused alternative to gridmv.py:251-348's broadcast): the last pass stores
+ * each output row into every node's next-iterate buffer (peer pointers, up
+ * to 8) at row row_off + row; sld_peer_barrier then signals every node's
+ * flag word (system-scope atomics) and waits for its own to reach target.
+ * Peer buffers cross processes as 64-byte CUDA IPC handles.
+ */
+int sld_mat_set_peers(sld_mat *m, int npeer, const uint64_t *yptrs, int64_t row_off);
+int sld_spmv_peers(sld_mat *m, uint64_t x_ptr);
+int sld_peer_barrier(sld_ctx *ctx, int npeer, const uint64_t *flag_ptrs, uint64_t my_flag, uint32_t target);
+int sld_dev_alloc(int device, int64_t bytes, uint64_t *ptr);
+int sld_dev_free(int device, uint64_t ptr);
+int sld_ipc_get(int device, uint64_t ptr, uint8_t *handle64);
+int sld_ipc_open(int device, const uint8_t *handle64, uint64_t *ptr);
+int sld_ipc_close(int device, uint64_t ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -195,6 +195,10 @@ struct sld_mat {
   int short_rows = 0;
   // die split (halves == 2): each pass's columns are dealt to the two dies
   int halves = 1;
+  // peer push (sld_mat_set_peers): next-iterate buffers of the r grid nodes
+  int npeer = 0;
+  uint32_t* yp[8] = {nullptr};
+  int64_t peer_off = 0;
   int64_t half_chunk = 0;      // columns per interleaved chunk
   unsigned split_grid = 0;     // persistent CTAs of the split kernel
   uint32_t* xch = nullptr;     // [nslots * G * SW]
@@ -1405,6 +1409,11 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
   a.has_full = (M->full_ptr && M->n_full) ? 1 : 0;
   a.policy = M->policy;
   a.pf = (uint32_t)M->pf;
+  if (!y && M->npeer) {
+    a.npeer = M->npeer;
+    for (int k = 0; k < M->npeer; k++) a.yp[k] = M->yp[k];
+    a.peer_off = M->peer_off;
+  }
   const LOps& o = ops(c->L);
   if (M->nslices == 0) {
     // no rows: still record the projection
@@ -1475,6 +1484,121 @@ extern "C" int sld_spmv(sld_mat* M, sld_vec* in, sld_vec* out) {
   launch_product(M, in->buf[in->cur], out->buf[out->cur], nullptr, 0, nullptr);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(M->ctx->stream));
+  return SLD_OK;
+}
+
+// ---- r x 1 grid with the all-gather fused into the SpMV epilogue: the last
+// pass stores each output row into every node's next iterate (peer device
+// pointers: cudaIpc handles across processes, NVLink P2P across GPUs), and
+// a flag barrier (system-scope atomics on every node's flag word) orders
+// the iterations.
+extern "C" int sld_mat_set_peers(sld_mat* M, int npeer, const uint64_t* yptrs, int64_t row_off) {
+  if (!M || npeer < 0 || npeer > 8 || (npeer && !yptrs) || row_off < 0)
+    return fail(SLD_E_ARG, "bad peer set (1..8 peers)");
+  if (npeer && (M->halves != 1 || M->sliced)) return fail(SLD_E_ARG, "peer push runs on the row-major layouts");
+  M->npeer = npeer;
+  for (int k = 0; k < 8; k++) M->yp[k] = k < npeer ? (uint32_t*)(uintptr_t)yptrs[k] : nullptr;
+  M->peer_off = row_off;
+  return SLD_OK;
+}
+
+// one product from the raw iterate x_ptr into the peers' buffers
+// (asynchronous on the context stream)
+extern "C" int sld_spmv_peers(sld_mat* M, uint64_t x_ptr) {
+  if (!M || !x_ptr || !M->npeer) return fail(SLD_E_ARG, "no peers set");
+  CU(cudaSetDevice(M->ctx->dev));
+  launch_product(M, (const uint32_t*)(uintptr_t)x_ptr, nullptr, nullptr, 0, nullptr);
+  CU(cudaGetLastError());
+  return SLD_OK;
+}
+
+namespace {
+struct PeerFlags {
+  uint32_t* f[8];
+};
+__global__ void peer_barrier_kernel(const PeerFlags pf, int npeer, const uint32_t* my_flag, uint32_t target,
+                                    int* timed_out) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int k = 0; k < npeer; k++) atomicAdd_system(pf.f[k], 1u);
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_flag) : "memory");
+    if ((int32_t)(v - target) >= 0) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 30000000000ull) {  // 30 s: a peer died; report instead of hanging
+      *timed_out = 1;
+      break;
+    }
+    __nanosleep(200);
+  }
+  __threadfence_system();
+}
+}  // namespace
+
+// signal every node (flag words, peer pointers, own included), then wait
+// until this node's flag reaches `target` (= npeer * iterations done)
+extern "C" int sld_peer_barrier(sld_ctx* c, int npeer, const uint64_t* flag_ptrs, uint64_t my_flag,
+                                uint32_t target) {
+  if (!c || npeer < 1 || npeer > 8 || !flag_ptrs || !my_flag) return fail(SLD_E_ARG, "bad barrier arguments");
+  CU(cudaSetDevice(c->dev));
+  static thread_local int* d_to = nullptr;
+  static thread_local int d_to_dev = -1;
+  if (!d_to || d_to_dev != c->dev) {
+    CU(cudaMalloc(&d_to, sizeof(int)));
+    d_to_dev = c->dev;
+  }
+  CU(cudaMemsetAsync(d_to, 0, sizeof(int), c->stream));
+  PeerFlags pf;
+  for (int k = 0; k < 8; k++) pf.f[k] = k < npeer ? (uint32_t*)(uintptr_t)flag_ptrs[k] : nullptr;
+  peer_barrier_kernel<<<1, 32, 0, c->stream>>>(pf, npeer, (const uint32_t*)(uintptr_t)my_flag, target, d_to);
+  CU(cudaGetLastError());
+  int to = 0;
+  CU(cudaMemcpyAsync(&to, d_to, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (to) return fail(SLD_E_CUDA, "peer barrier timed out (a grid node stopped)");
+  return SLD_OK;
+}
+
+// raw device memory and CUDA IPC handles (64 bytes) for the peer buffers
+extern "C" int sld_dev_alloc(int device, int64_t bytes, uint64_t* ptr) {
+  if (!ptr || bytes <= 0) return fail(SLD_E_ARG, "bad allocation");
+  CU(cudaSetDevice(device));
+  void* p = nullptr;
+  CU(cudaMalloc(&p, (size_t)bytes));
+  CU(cudaMemset(p, 0, (size_t)bytes));
+  *ptr = (uint64_t)(uintptr_t)p;
+  return SLD_OK;
+}
+extern "C" int sld_dev_free(int device, uint64_t ptr) {
+  CU(cudaSetDevice(device));
+  if (ptr) CU(cudaFree((void*)(uintptr_t)ptr));
+  return SLD_OK;
+}
+extern "C" int sld_ipc_get(int device, uint64_t ptr, uint8_t* handle64) {
+  if (!ptr || !handle64) return fail(SLD_E_ARG, "null argument");
+  CU(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)ptr));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memcpy(handle64, &h, 64);
+  return SLD_OK;
+}
+extern "C" int sld_ipc_open(int device, const uint8_t* handle64, uint64_t* ptr) {
+  if (!handle64 || !ptr) return fail(SLD_E_ARG, "null argument");
+  CU(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  void* p = nullptr;
+  CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr = (uint64_t)(uintptr_t)p;
+  return SLD_OK;
+}
+extern "C" int sld_ipc_close(int device, uint64_t ptr) {
+  CU(cudaSetDevice(device));
+  if (ptr) CU(cudaIpcCloseMemHandle((void*)(uintptr_t)ptr));
   return SLD_OK;
 }
 

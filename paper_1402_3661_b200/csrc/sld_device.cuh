@@ -70,6 +70,11 @@ struct SpmvArgs {
   uint32_t* cnt;           // [nslices] arrival counters (parity = order)
   uint32_t* queue;         // [3] work queue per die + exit counter
   uint32_t pf;             // index groups prefetched into L2 ahead of use
+  // peer push (r x 1 grid, last pass): each output row goes to every node's
+  // next-iterate buffer (peer memory) at row peer_off + row, instead of y
+  uint32_t* yp[8];
+  int npeer;
+  int64_t peer_off;
 };
 
 // ---------------------------------------------------------------- loads
@@ -453,6 +458,14 @@ __device__ __forceinline__ void store_row(const SpmvArgs& a, int64_t slot, int c
     if (row < 0) return;
 #pragma unroll
     for (int i = 0; i < SW; i++) o[i] = i < L ? (Rr[i] ^ 0x80000000u) : 0u;
+    if (a.npeer) {
+      // NVLink peer stores (or same-device buffers): the all-gather of the
+      // r x 1 grid done by the SpMV epilogue itself
+#pragma unroll 1
+      for (int k = 0; k < a.npeer; k++)
+        store_slot<SW>(a.yp[k] + ((size_t)(a.peer_off + row) * G + chain) * SW, o);
+      return;
+    }
     uint32_t* dst = a.y + ((size_t)row * G + chain) * SW;
     if (a.policy & 2) store_slot_hint<SW>(dst, o, pol);
     else store_slot<SW>(dst, o);
