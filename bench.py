@@ -18,6 +18,7 @@ matrix, rank 0 only.
 """
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -260,21 +261,26 @@ def run_grid(args, cfg, rank, world, local, dist, log):
     A, _, mod = build_matrix(cfg, log)
     t = time.time()
     perm = balance_permutation(A, g)
-    fused = g.c == 1 and args.grid_impl == "peer"
+    fused = args.grid_impl == "peer"
     if fused:
-        # r x 1: the all-gather fused into the SpMV epilogue (peer stores +
-        # flag barrier, paper_1402_3661_b200/peergrid.py)
+        # exchanges done by the nodes over peer memory (paper_1402_3661_b200/
+        # peergrid.py): r x 1 -- the all-gather fused into the SpMV epilogue;
+        # r x c -- partials pushed into the row collector by the epilogue,
+        # reduced, scattered by P2P copies.  Flag barriers, no collective.
         from paper_1402_3661_b200 import _native as N
-        from paper_1402_3661_b200.peergrid import PeerRowGrid
+        from paper_1402_3661_b200.peergrid import PeerGrid, PeerRowGrid
         torch.cuda.set_device(local)
 
         def exchange(obj):
             out = [None] * world
             tdist.all_gather_object(out, obj)
             return out
-        grid = PeerRowGrid(A, g.r, rank, exchange, device=local, perm=perm)
+        if g.c == 1:
+            grid = PeerRowGrid(A, g.r, rank, exchange, device=local, perm=perm)
+        else:
+            grid = PeerGrid(A, g, rank, exchange, device=local, perm=perm)
         N.check(N.load().sld_ctx_set_stream(grid.field.handle, torch.cuda.current_stream(local).cuda_stream))
-        log(f"peer-push grid {g} node {rank} block built in {time.time() - t:.1f}s")
+        log(f"peer grid {g} node {rank} block built in {time.time() - t:.1f}s")
     else:
         grid = B200Grid(A, g, GridComm(g), device=local, perm=perm)
         log(f"grid {g} node {(grid.i, grid.j)} block built in {time.time() - t:.1f}s")
@@ -295,10 +301,15 @@ def run_grid(args, cfg, rank, world, local, dist, log):
     tdist.all_reduce(t_all, op=tdist.ReduceOp.MAX)
     ms = float(t_all.item())
     if fused:
-        W = 4 * mod.limbs
-        comm = {"impl": "SpMV epilogue peer stores + flag barrier (no collective)",
-                "bytes_per_iter_reference_accounting": (g.r - 1) * grid.n_padded * mod.byte_width,
-                "wire_bytes_per_iter": (g.r - 1) * grid.n_padded * 32 * ((W + 31) // 32),
+        from paper_1402_3661_b200.balance import comm_volume_model
+        q = math.lcm(g.r, g.c)
+        frag_rows = grid.n_padded // q
+        slot_bytes = 32 * ((4 * mod.limbs + 31) // 32)
+        comm = {"impl": ("SpMV epilogue peer stores + flag barrier" if g.c == 1 else
+                         "epilogue peer stores into the collector + add_mod + P2P copies + flag barriers")
+                        + " (no collective)",
+                "bytes_per_iter_reference_accounting": comm_volume_model(g, frag_rows * mod.byte_width),
+                "wire_bytes_per_iter": comm_volume_model(g, frag_rows * slot_bytes),
                 "messages_per_iter": 0}
         stripes = grid.dm.info()["stripes"]
     else:
@@ -317,13 +328,15 @@ def run_grid(args, cfg, rank, world, local, dist, log):
         "scaling": "strong", "vs_baseline": None, "dtype": "u32 limbs, exact mod l",
         "data": "synthetic (native corpus generator, FFS profile, seed 1)",
         "config": dict(config_block("cfg4", cfg, A, mod, world), grid=str(g),
-                       parallelism=(f"one chain on a {g} grid, all-gather fused into the SpMV (peer stores)"
+                       parallelism=(f"one chain on a {g} grid, exchanges over peer memory (no collective)"
                                     if fused else f"one chain on a {g} grid (NCCL p2p / all-gather)")),
         "roofline": {"bound": "hbm", "achieved": B / world / (per / 1e3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": B / world / (per / 1e3) / 1e9 / peak, "traffic": None,
                      "peak_kind": peak_kind},
         "comm": comm,
-        "gpu_launches": args.steps * (stripes + (1 if (g.c > 1 or fused) else 0)),
+        # rank 0 (a row collector): SpMV passes, add_mod when c > 1, and the
+        # flag barriers of the peer exchange (1 for r x 1, 2 for r x c)
+        "gpu_launches": args.steps * (stripes + (1 if g.c > 1 else 0) + ((1 if g.c == 1 else 2) if fused else 0)),
         "clocks": clk.summary(),
     }
     if rank == 0:
@@ -362,7 +375,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--grid", default=None, help="cfg4 grid RxC (default: <gpus>x1)")
     ap.add_argument("--grid-impl", default="peer", choices=["peer", "nccl"],
-                    help="cfg4 r x 1 exchange: fused peer stores (default) or the NCCL node protocol")
+                    help="cfg4 exchange: over peer memory (default) or the NCCL node protocol")
     ap.add_argument("--chains", type=int, default=None,
                     help="Krylov chains advanced per matrix pass on each GPU (1, 2, 4)")
     args = ap.parse_args()

@@ -270,6 +270,7 @@ int sld_sldv_read(const char *path, uint32_t *limbs, int stride);
 int sld_mat_set_peers(sld_mat *m, int npeer, const uint64_t *yptrs, int64_t row_off);
 int sld_spmv_peers(sld_mat *m, uint64_t x_ptr);
 int sld_peer_barrier(sld_ctx *ctx, int npeer, const uint64_t *flag_ptrs, uint64_t my_flag, uint32_t target);
+int sld_memcpy_async(sld_ctx *ctx, uint64_t dst, uint64_t src, int64_t bytes);
 int sld_dev_alloc(int device, int64_t bytes, uint64_t *ptr);
 int sld_dev_free(int device, uint64_t ptr);
 int sld_ipc_get(int device, uint64_t ptr, uint8_t *handle64);

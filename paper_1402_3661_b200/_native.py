@@ -33,7 +33,7 @@ EXPORTS = [
     "sld_vec_upload_limbs", "sld_vec_download_limbs", "sld_vec_device_ptr",
     "sld_vec_upload_planes_chains", "sld_vec_download_planes_chains",
     "sld_lcset_create", "sld_lcset_apply", "sld_lcset_destroy",
-    "sld_mat_set_peers", "sld_spmv_peers", "sld_peer_barrier", "sld_dev_alloc", "sld_dev_free",
+    "sld_mat_set_peers", "sld_spmv_peers", "sld_peer_barrier", "sld_memcpy_async", "sld_dev_alloc", "sld_dev_free",
     "sld_ipc_get", "sld_ipc_open", "sld_ipc_close",
     "sld_spmv", "sld_spmv_planes", "sld_krylov_unit",
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
@@ -101,6 +101,7 @@ def load(build_if_missing=False):
             "sld_mat_set_peers": ([vp, i32, vp, i64], i32),
             "sld_spmv_peers": ([vp, ctypes.c_uint64], i32),
             "sld_peer_barrier": ([vp, i32, vp, ctypes.c_uint64, ctypes.c_uint32], i32),
+            "sld_memcpy_async": ([vp, ctypes.c_uint64, ctypes.c_uint64, i64], i32),
             "sld_dev_alloc": ([i32, i64, vp], i32),
             "sld_dev_free": ([i32, ctypes.c_uint64], i32),
             "sld_ipc_get": ([i32, ctypes.c_uint64, vp], i32),

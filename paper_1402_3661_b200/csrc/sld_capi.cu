@@ -1562,6 +1562,15 @@ extern "C" int sld_peer_barrier(sld_ctx* c, int npeer, const uint64_t* flag_ptrs
   return SLD_OK;
 }
 
+// stream-ordered device copy (peer pointers included: an NVLink P2P copy)
+extern "C" int sld_memcpy_async(sld_ctx* c, uint64_t dst, uint64_t src, int64_t bytes) {
+  if (!c || (bytes && (!dst || !src)) || bytes < 0) return fail(SLD_E_ARG, "bad copy");
+  CU(cudaSetDevice(c->dev));
+  if (bytes) CU(cudaMemcpyAsync((void*)(uintptr_t)dst, (const void*)(uintptr_t)src, (size_t)bytes,
+                                cudaMemcpyDeviceToDevice, c->stream));
+  return SLD_OK;
+}
+
 // raw device memory and CUDA IPC handles (64 bytes) for the peer buffers
 extern "C" int sld_dev_alloc(int device, int64_t bytes, uint64_t* ptr) {
   if (!ptr || bytes <= 0) return fail(SLD_E_ARG, "bad allocation");
