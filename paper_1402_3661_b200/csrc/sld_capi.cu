@@ -828,7 +828,7 @@ extern "C" int sld_lcset_create(sld_ctx* c, const uint64_t* y_ptrs, int n, int64
   S->n = n;
   S->rows = rows;
   S->mtiles = (rows + 127) / 128;
-  S->grid = (int)std::max<int64_t>(1, std::min<int64_t>(S->mtiles, c->sms));
+  S->grid = (int)std::max<int64_t>(1, std::min<int64_t>(S->mtiles, (int64_t)TCL_CTAS_PER_SM * c->sms));
   CU(cudaMalloc(&S->Y, std::max<size_t>((size_t)S->mtiles * tcl_ytile_bytes(n), 16)));
   uint64_t* dptrs = nullptr;
   CU(cudaMalloc(&dptrs, 8 * n));

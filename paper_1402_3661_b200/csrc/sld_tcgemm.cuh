@@ -332,6 +332,9 @@ constexpr int TCL_N = 64;                       // byte positions k of the produ
 constexpr uint32_t TCL_IDESC = (2u << 4) | ((uint32_t)(TCL_N >> 3) << 17) | ((128u >> 4) << 24);
 constexpr int TCL_STAGES = 3;
 constexpr int TCL_THREADS = 192;
+#ifndef TCL_CTAS_PER_SM
+#define TCL_CTAS_PER_SM 2  // two CTAs per SM: twice the epilogue warps (smem 2 x ~113 KB, TMEM 2 x 128 cols)
+#endif
 
 __host__ __device__ constexpr int tcl_ytile_bytes(int n) { return 128 * 32 * n; }
 __host__ __device__ constexpr int tcl_b_bytes(int n) { return TCL_N * 32 * n; }
@@ -374,7 +377,7 @@ struct TclCoef {
 };
 
 template <int L>
-__global__ void __launch_bounds__(TCL_THREADS, 1)
+__global__ void __launch_bounds__(TCL_THREADS, TCL_CTAS_PER_SM)
     tcl_combine(const uint8_t* __restrict__ Y, const TclCoef cf, int n, int64_t rows,
                 int64_t mtiles, const uint32_t* __restrict__ acc, uint32_t* __restrict__ dst,
                 const uint32_t* __restrict__ fold, const ModParams mp) {
