@@ -225,6 +225,22 @@ int sld_corpus_fill(int64_t n, int64_t ncols, double decay, double pm1, int64_t 
                     int64_t *small_vals, int nthreads);
 
 /*
+ * Grid partition builder (host code): block (bi, bj) of the r x c split of
+ * B = P_r A P_c^T -- replaces sldlag/balance.py split (201-242) and
+ * permuted_padded (245-267, the r = c = 1 case).  Entries are A's CSR
+ * (index k < nnz; col_idx of col_bytes 4 or 8) followed by n_extra entries
+ * given in permuted coordinates (dense-column nonzeros, then the pinned +1
+ * padding; index nnz + e).  Pass 1 (src == NULL) fills rp[0..n_pad/r] and
+ * returns the block's entry count; pass 2 fills src[] and lc[] (local
+ * column), each local row ordered by (lc, src).  threads <= 0: all cores.
+ */
+int64_t sld_split_block(int64_t nrows, const int64_t *row_ptr, const void *col_idx, int col_bytes,
+                        const int64_t *row_perm, const int64_t *col_perm, int64_t n_extra,
+                        const int64_t *extra_r, const int64_t *extra_c, int64_t n_pad, int32_t r,
+                        int32_t c, int32_t bi, int32_t bj, int64_t *rp, int64_t *src, int32_t *lc,
+                        int32_t threads);
+
+/*
  * Native file formats of the reference (host code, no device needed).
  *
  * SLDM matrix (sldlag/spmatrix.py:14-22, store_matrix/load_matrix 358-436).

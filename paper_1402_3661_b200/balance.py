@@ -11,6 +11,8 @@ Restates sldlag/balance.py:32-267:
     coordinate (balance.py:201-242);
   * `permuted_padded` -- the assembled matrix the grid computes with
     (balance.py:245-267), the parity reference for the grid.
+Blocks are cut by the native builder (csrc/sld_split.cpp): a per-row
+counting sort that yields the reference lexsort's order.
 The permutations are pinned against the reference's own output in
 tests/golden/grid_cases.npz.
 """
@@ -141,43 +143,69 @@ def identity_permutation(A, g: GridSpec) -> PermutationPair:
     return PermutationPair(e, e.copy(), A.nrows)
 
 
-def _all_entries(A):
-    """(rows, cols, tags, smalls, {flat index: full value}) with dense columns
-    materialised as full entries after the sparse ones."""
+def _extra_entries(A, p: PermutationPair):
+    """The entries of B outside A's CSR, in permuted coordinates and in the
+    reference's order: dense-column nonzeros as full entries (column by
+    column, rows ascending), then one pinned +1 per padded coordinate."""
     from .modring import limbs_to_ints
-    rows = np.repeat(np.arange(A.nrows, dtype=np.int64), np.diff(A.row_ptr))
-    cols = np.asarray(A.col_idx, dtype=np.int64)
-    tags = np.asarray(A.tags, dtype=np.uint8)
-    smalls = np.asarray(A.small_vals, dtype=np.int64)
-    fulls = dict(A.full_vals)
-    if A.dense_cols:
-        er, ec, ev = [], [], []
-        for gidx, col in A.dense_cols:
-            vals = limbs_to_ints(col) if isinstance(col, np.ndarray) else list(col)
-            for i, v in enumerate(vals):
-                if v:
-                    er.append(i)
-                    ec.append(gidx)
-                    ev.append(v)
-        base = len(rows)
-        rows = np.concatenate([rows, np.array(er, dtype=np.int64)])
-        cols = np.concatenate([cols, np.array(ec, dtype=np.int64)])
-        tags = np.concatenate([tags, np.full(len(er), TAG_FULL, dtype=np.uint8)])
-        smalls = np.concatenate([smalls, np.zeros(len(er), dtype=np.int64)])
-        for k, v in enumerate(ev):
-            fulls[base + k] = v
-    return rows, cols, tags, smalls, fulls
-
-
-def _permuted_entries(A, p: PermutationPair):
-    rows, cols, tags, smalls, fulls = _all_entries(A)
-    nr, nc = p.row_perm[rows], p.col_perm[cols]
+    er, ec, ev = [], [], []
+    for gidx, col in A.dense_cols:
+        vals = limbs_to_ints(col) if isinstance(col, np.ndarray) else list(col)
+        for i, v in enumerate(vals):
+            if v:
+                er.append(i)
+                ec.append(gidx)
+                ev.append(v)
+    er = p.row_perm[np.array(er, dtype=np.int64)]
+    ec = p.col_perm[np.array(ec, dtype=np.int64)]
     pad = np.arange(A.nrows, p.n_padded, dtype=np.int64)
-    nr = np.concatenate([nr, pad])
-    nc = np.concatenate([nc, pad])
-    tags = np.concatenate([tags, np.full(len(pad), TAG_PLUS_ONE, dtype=np.uint8)])
-    smalls = np.concatenate([smalls, np.ones(len(pad), dtype=np.int64)])
-    return nr, nc, tags, smalls, fulls
+    rows = np.concatenate([er, pad])
+    cols = np.concatenate([ec, pad])
+    tags = np.concatenate([np.full(len(ev), TAG_FULL, dtype=np.uint8),
+                           np.full(len(pad), TAG_PLUS_ONE, dtype=np.uint8)])
+    smalls = np.concatenate([np.zeros(len(ev), dtype=np.int64), np.ones(len(pad), dtype=np.int64)])
+    return rows, cols, tags, smalls, ev
+
+
+def _block(A, p: PermutationPair, n_pad: int, r: int, c: int, i: int, j: int, extra) -> SparseMatrix:
+    """Block (i, j) of the r x c split of P_r A P_c^T, built natively
+    (csrc/sld_split.cpp): a per-row counting sort, rows ordered by (local
+    column, entry index) -- the order of the reference's lexsort."""
+    from . import _native as N
+    lib = N.load()
+    er, ec, etags, esmalls, evals = extra
+    col = np.ascontiguousarray(A.col_idx)
+    if col.dtype not in (np.int32, np.int64):
+        col = col.astype(np.int64)
+    row_ptr = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+    br, bc = n_pad // r, n_pad // c
+    rp = np.zeros(br + 1, dtype=np.int64)
+    args = (A.nrows, N.ptr(row_ptr), N.ptr(col), col.dtype.itemsize, N.ptr(p.row_perm), N.ptr(p.col_perm),
+            len(er), N.ptr(er), N.ptr(ec), n_pad, r, c, i, j, N.ptr(rp))
+    nb = lib.sld_split_block(*args, None, None, 0)
+    if nb < 0:
+        N.check(int(nb))
+    src = np.empty(nb, dtype=np.int64)
+    lc = np.empty(nb, dtype=np.int32)
+    N.check(int(min(0, lib.sld_split_block(*args, N.ptr(src), N.ptr(lc), 0))))
+    nnz = len(A.col_idx)
+    inner = src < nnz
+    tags = np.empty(nb, dtype=np.uint8)
+    smalls = np.empty(nb, dtype=np.int64)
+    if inner.all():
+        tags[:] = np.asarray(A.tags)[src]
+        smalls[:] = np.asarray(A.small_vals)[src]
+    else:
+        si, so = src[inner], src[~inner] - nnz
+        tags[inner] = np.asarray(A.tags)[si]
+        smalls[inner] = np.asarray(A.small_vals)[si]
+        tags[~inner] = etags[so]
+        smalls[~inner] = esmalls[so]
+    fulls = {}
+    for t in np.nonzero(tags == TAG_FULL)[0]:
+        k = int(src[t])
+        fulls[int(t)] = A.full_vals[k] if k < nnz else evals[k - nnz]
+    return SparseMatrix(A.mod, br, bc, rp, lc, tags, smalls, fulls, validate=False)
 
 
 class BlockSplit:
@@ -202,38 +230,20 @@ def split(A, p: PermutationPair, g: GridSpec, only=None) -> BlockSplit:
     n_pad = padded_size(A.nrows, g)
     if p.n_padded != n_pad:
         raise ValueError("permutation size does not match padded size")
-    br, bc = n_pad // g.r, n_pad // g.c
-    nr, nc, tags, smalls, fulls = _permuted_entries(A, p)
-    src = np.arange(len(nr), dtype=np.int64)
-    bi, bj = nr // br, nc // bc
-    order = np.lexsort((nc % bc, nr % br, bj, bi))
-    bi, bj, lr, lc, src = bi[order], bj[order], (nr % br)[order], (nc % bc)[order], src[order]
-    tags_s, smalls_s = tags[order], smalls[order]
-    bounds = np.searchsorted(bi * g.c + bj, np.arange(g.r * g.c + 1))
+    extra = _extra_entries(A, p)
     blocks = [[None] * g.c for _ in range(g.r)]
     for i in range(g.r):
         for j in range(g.c):
-            if only is not None and (i, j) not in only:
-                continue
-            lo, hi = bounds[i * g.c + j], bounds[i * g.c + j + 1]
-            fl = {int(t): fulls[int(src[lo + t])] for t in np.nonzero(tags_s[lo:hi] == TAG_FULL)[0]}
-            rp = np.zeros(br + 1, dtype=np.int64)
-            np.cumsum(np.bincount(lr[lo:hi], minlength=br), out=rp[1:])
-            blocks[i][j] = SparseMatrix(A.mod, br, bc, rp, lc[lo:hi].astype(np.int32), tags_s[lo:hi],
-                                        smalls_s[lo:hi], fl, validate=False)
+            if only is None or (i, j) in only:
+                blocks[i][j] = _block(A, p, n_pad, g.r, g.c, i, j, extra)
     return BlockSplit(blocks, g, A.nrows, n_pad)
 
 
 def permuted_padded(A, p: PermutationPair, g: GridSpec) -> SparseMatrix:
     n_pad = padded_size(A.nrows, g)
-    nr, nc, tags, smalls, fulls = _permuted_entries(A, p)
-    src = np.arange(len(nr), dtype=np.int64)
-    order = np.lexsort((nc, nr))
-    nr, nc, tags, smalls, src = nr[order], nc[order], tags[order], smalls[order], src[order]
-    fl = {int(t): fulls[int(src[t])] for t in np.nonzero(tags == TAG_FULL)[0]}
-    rp = np.zeros(n_pad + 1, dtype=np.int64)
-    np.cumsum(np.bincount(nr, minlength=n_pad), out=rp[1:])
-    return SparseMatrix(A.mod, n_pad, n_pad, rp, nc.astype(np.int32), tags, smalls, fl, validate=False)
+    if p.n_padded != n_pad:
+        raise ValueError("permutation size does not match padded size")
+    return _block(A, p, n_pad, 1, 1, 0, 0, _extra_entries(A, p))
 
 
 def block_nnz(bs: BlockSplit) -> np.ndarray:
