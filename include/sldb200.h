@@ -205,6 +205,18 @@ int sld_xblock_destroy(sld_xblock *x);
 int sld_krylov_dense(sld_mat *m, sld_vec *v, sld_xblock *x, int64_t steps, uint32_t *terms_limbs);
 
 /*
+ * Mksol Horner step fused into one product (sldlag/solver.py:522-536,
+ * planes_scalar_mul_mod + planes_add_mod of vecops.py:261-278):
+ * sld_mat_mksol_bind copies n <= 8 y vectors into the matrix's slot order
+ * (n = 0 releases them); sld_spmv_mksol then computes
+ * out = A in + sum_s coeffs[s] y_s mod l (coeffs: n x L canonical limbs),
+ * the combination in the last pass's epilogue.  Needs L <= 8 and the
+ * one-chain pass layout (SLD_E_ARG otherwise).  Asynchronous.
+ */
+int sld_mat_mksol_bind(sld_mat *m, sld_vec *const *ys, int n);
+int sld_spmv_mksol(sld_mat *m, sld_vec *in, sld_vec *out, const uint32_t *coeffs);
+
+/*
  * Timing hook for bench.py: runs `steps` products v <- A v on device
  * (ping-pong, graph-captured) and returns device milliseconds measured
  * with CUDA events on the context stream; kernel_ms gets the average

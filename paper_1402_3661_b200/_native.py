@@ -39,7 +39,7 @@ EXPORTS = [
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
     "sld_bench_spmv", "sld_corpus_rows", "sld_corpus_fill",
     "sld_sldm_info", "sld_sldm_read", "sld_sldm_write", "sld_sldv_write", "sld_sldv_info", "sld_sldv_read",
-    "sld_split_block",
+    "sld_split_block", "sld_mat_mksol_bind", "sld_spmv_mksol",
 ]
 
 
@@ -128,6 +128,8 @@ def load(build_if_missing=False):
             "sld_corpus_rows": ([i64, i64, ctypes.c_double, ctypes.c_uint64, vp], i32),
             "sld_corpus_fill": ([i64, i64, ctypes.c_double, ctypes.c_double, i64, ctypes.c_uint64,
                                  vp, vp, vp, vp, i32], i32),
+            "sld_mat_mksol_bind": ([vp, vp, i32], i32),
+            "sld_spmv_mksol": ([vp, vp, vp, vp], i32),
             "sld_split_block": ([i64, vp, vp, i32, vp, vp, i64, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, i32],
                                 i64),
         }

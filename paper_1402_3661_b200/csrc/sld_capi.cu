@@ -217,6 +217,9 @@ struct sld_mat {
   // dense-X scratch
   uint64_t* dproj_part = nullptr;
   size_t dproj_cap = 0;
+  // fused Mksol step (sld_mat_mksol_bind): y vectors in slot order
+  uint32_t* mk_y = nullptr;
+  int mk_n = 0;
 };
 
 // -------------------------------------------------- per-L dispatch table
@@ -948,7 +951,7 @@ static void mat_free(sld_mat* m) {
   if (!m) return;
   void* ptrs[] = {m->slices, m->pm_idx, m->s_idx, m->s_coef, m->slot_row, m->lane_k4, m->full_ptr,
                   m->full_col, m->full_val, m->dense_val, m->part, m->stage, m->proj_rows,
-                  m->terms_dev, m->dproj_part, m->xch, m->cnt, m->queue};
+                  m->terms_dev, m->dproj_part, m->xch, m->cnt, m->queue, m->mk_y};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->tmp_in) sld_vec_destroy(m->tmp_in);
@@ -1383,7 +1386,7 @@ extern "C" int sld_mat_info(const sld_mat* m, int64_t* info) {
 
 // launch all stripe passes of one product on the context stream
 static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows,
-                           int proj_m, uint32_t* terms_out) {
+                           int proj_m, uint32_t* terms_out, const uint32_t* mk_coeffs = nullptr) {
   sld_ctx* c = M->ctx;
   SpmvArgs a;
   memset(&a, 0, sizeof(a));
@@ -1413,6 +1416,13 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
     a.npeer = M->npeer;
     for (int k = 0; k < M->npeer; k++) a.yp[k] = M->yp[k];
     a.peer_off = M->peer_off;
+  }
+  if (mk_coeffs) {
+    a.mk_y = M->mk_y;
+    a.mk_n = M->mk_n;
+    a.fold = c->fold;
+    for (int s = 0; s < M->mk_n; s++)
+      for (int i = 0; i < c->L; i++) a.mk_c[s][i] = mk_coeffs[(size_t)s * c->L + i];
   }
   const LOps& o = ops(c->L);
   if (M->nslices == 0) {
@@ -1461,7 +1471,8 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
       v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
     }
-    o.pass(M->chains, p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
+    if (mk_coeffs && p == M->npass - 1) o.pass_mk(p == 0, M->nslices, c->stream, a, c->mp);
+    else o.pass(M->chains, p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
   }
   if (M->apw && c->apw_max) {
     cudaStreamAttrValue v;
@@ -1484,6 +1495,51 @@ extern "C" int sld_spmv(sld_mat* M, sld_vec* in, sld_vec* out) {
   launch_product(M, in->buf[in->cur], out->buf[out->cur], nullptr, 0, nullptr);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(M->ctx->stream));
+  return SLD_OK;
+}
+
+// ---- Mksol's Horner step in one product (solver.py:522-536): bind the n <= 8
+// y vectors once (canonical copies in the slot order of the passes), then
+// each step is out = A in + sum_s coeffs[s] y_s with the combination in the
+// last pass's epilogue.  One-chain pass layout only (not short rows, limb
+// slicing or the die split): the caller combines separately otherwise.
+extern "C" int sld_mat_mksol_bind(sld_mat* M, sld_vec* const* ys, int n) {
+  if (!M || n < 0 || n > 8 || (n && !ys)) return fail(SLD_E_ARG, "bad Mksol binding (0..8 vectors)");
+  sld_ctx* c = M->ctx;
+  CU(cudaSetDevice(c->dev));
+  if (M->mk_y) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(M->mk_y);
+    M->mk_y = nullptr;
+    M->mk_n = 0;
+  }
+  if (!n) return SLD_OK;
+  if (c->L > 8 || M->chains != 1 || M->halves != 1 || M->sliced || M->short_rows)
+    return fail(SLD_E_ARG, "fused Mksol step needs the one-chain pass layout and ell < 2^256");
+  for (int s = 0; s < n; s++) {
+    if (!ys[s] || ys[s]->ctx != c || ys[s]->chains != 1) return fail(SLD_E_ARG, "bad Mksol vector %d", s);
+    if (ys[s]->n < M->nrows) return fail(SLD_E_ARG, "Mksol vector %d shorter than the matrix rows", s);
+  }
+  const size_t per = (size_t)M->nslots * c->SW;
+  CU(cudaMalloc(&M->mk_y, std::max<size_t>(per * n * 4, 16)));
+  for (int s = 0; s < n; s++) ops(c->L).mk_gather(ys[s]->buf[ys[s]->cur], M->slot_row, M->nslots, M->mk_y + per * s,
+                                                  c->stream);
+  M->mk_n = n;
+  CU(cudaGetLastError());
+  return SLD_OK;
+}
+
+// out = A in + sum_s coeffs[s] y_s mod ell (coeffs: mk_n x L canonical limbs).
+// Asynchronous on the context stream.
+extern "C" int sld_spmv_mksol(sld_mat* M, sld_vec* in, sld_vec* out, const uint32_t* coeffs) {
+  if (!M || !in || !out || !coeffs) return fail(SLD_E_ARG, "null argument");
+  if (!M->mk_n) return fail(SLD_E_ARG, "no Mksol vectors bound");
+  if (in->n != M->total_cols || out->n < M->nrows || in == out || in->ctx != M->ctx || out->ctx != M->ctx ||
+      in->chains != 1 || out->chains != 1)
+    return fail(SLD_E_ARG, "bad Mksol step vectors");
+  CU(cudaSetDevice(M->ctx->dev));
+  launch_product(M, in->buf[in->cur], out->buf[out->cur], nullptr, 0, nullptr, coeffs);
+  CU(cudaGetLastError());
   return SLD_OK;
 }
 

@@ -75,6 +75,12 @@ struct SpmvArgs {
   uint32_t* yp[8];
   int npeer;
   int64_t peer_off;
+  // fused Mksol Horner step (spmv_pass<L, 1, *, true, true>, L <= 8): the
+  // output row becomes (A w)[row] + sum_s mk_c[s] y_s[row] mod ell
+  const uint32_t* mk_y;  // [mk_n][nslots][SW] canonical y_s in the slot order
+  const uint32_t* fold;  // 2^(32k) mod ell for k = L .. 2L, L words each
+  int mk_n;
+  uint32_t mk_c[8][8];  // the step's coefficients, canonical, L limbs each
 };
 
 // ---------------------------------------------------------------- loads
@@ -478,7 +484,62 @@ __device__ __forceinline__ void store_row(const SpmvArgs& a, int64_t slot, int c
   }
 }
 
-template <int L, int G, bool FIRST, bool LAST>
+// Mksol's combination fused into the last pass (solver.py:522-536): R <-
+// R + sum_s c_s y_s[slot] mod ell.  32 x 32-bit limb products go lazily into
+// 64-bit columns (low word to column p+q, high word to p+q+1: < 2^40 for
+// n <= 8), are carried into 2L+1 limbs, the limbs above L folded with
+// 2^(32k) mod ell, and one more finalize reduces (|V| < (L+2) 2^32 ell).
+// The y_s are stored in slot order, so a warp's loads are coalesced.
+template <int L>
+__device__ __forceinline__ void mk_combine(const SpmvArgs& a, int64_t slot, const ModParams& mp, uint64_t pol,
+                                           uint32_t (&Rr)[L]) {
+  constexpr int SW = stride_words(L);
+  uint64_t col[2 * L];
+#pragma unroll
+  for (int k = 0; k < 2 * L; k++) col[k] = k < L ? Rr[k] : 0u;
+#pragma unroll
+  for (int s = 0; s < 8; s++) {
+    if (s >= a.mk_n) break;
+    uint32_t u[SW];
+    load_slot<SW>(a.mk_y + ((size_t)s * a.nslots + slot) * SW, u, pol);
+#pragma unroll
+    for (int p = 0; p < L; p++) {
+      const uint32_t c = a.mk_c[s][p];
+#pragma unroll
+      for (int q = 0; q < L; q++) {
+        const uint64_t pr = (uint64_t)c * u[q];
+        col[p + q] += (uint32_t)pr;
+        col[p + q + 1] += pr >> 32;
+      }
+    }
+  }
+  uint32_t V[2 * L];
+  uint64_t carry = 0;
+#pragma unroll
+  for (int k = 0; k < 2 * L; k++) {
+    const uint64_t t = col[k] + carry;
+    V[k] = (uint32_t)t;
+    carry = t >> 32;
+  }
+  int64_t acc[L + 1];
+#pragma unroll
+  for (int j = 0; j < L; j++) acc[j] = V[j];
+  acc[L] = 0;
+#pragma unroll
+  for (int k = L; k <= 2 * L; k++) {
+    const uint32_t limb = k < 2 * L ? V[k] : (uint32_t)carry;
+    const uint32_t* R = a.fold + (size_t)(k - L) * L;
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+      const uint64_t pr = (uint64_t)limb * __ldg(R + j);
+      acc[j] += (int64_t)(uint32_t)pr;
+      acc[j + 1] += (int64_t)(pr >> 32);
+    }
+  }
+  finalize<L>(acc, 0, mp, Rr);
+}
+
+template <int L, int G, bool FIRST, bool LAST, bool MK = false>
 __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const SpmvArgs a, const ModParams mp) {
   constexpr int SW = stride_words(L);
   constexpr int R = 32 / G;  // rows per warp = slice height
@@ -512,7 +573,23 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
   if (LAST && a.has_full) row_full<L, G>(a, mp, slot, a.slot_row[slot], xc, acc);
   uint32_t Rr[L];
   finalize<L>(acc, S, mp, Rr);
+  if constexpr (MK) mk_combine<L>(a, slot, mp, pol, Rr);
   store_row<L, G, LAST>(a, slot, chain, Rr, pol);
+}
+
+// canonical copy of y (biased, row-indexed) in the slot order of a matrix's
+// passes; padding slots are zero (the fused Mksol step's operand)
+template <int L>
+__global__ void mk_slot_gather(const uint32_t* __restrict__ y, const int32_t* __restrict__ slot_row, int64_t nslots,
+                               uint32_t* __restrict__ out) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nslots) return;
+  const int32_t row = slot_row[i];
+  uint32_t o[SW];
+#pragma unroll
+  for (int j = 0; j < SW; j++) o[j] = (row >= 0 && j < L) ? (y[(size_t)row * SW + j] ^ 0x80000000u) : 0u;
+  store_slot<SW>(out + (size_t)i * SW, o);
 }
 
 // ---------------------------------------------------- short-row SpMV pass

@@ -46,6 +46,10 @@ struct LOps {
   void (*read_rows)(const uint32_t*, const int64_t*, int, uint32_t*, cudaStream_t);
   void (*lincomb)(const LinCombArgs&, const ModParams&, cudaStream_t);
   void (*nonzero)(const uint32_t*, int64_t, int*, cudaStream_t);
+  // fused Mksol step: last pass of a one-chain product with the combination
+  // in its epilogue; slot-order copy of a y vector (false: L > 8)
+  bool (*pass_mk)(int first, int64_t nslices, cudaStream_t s, const SpmvArgs& a, const ModParams& mp);
+  bool (*mk_gather)(const uint32_t* y, const int32_t* slot_row, int64_t nslots, uint32_t* out, cudaStream_t s);
 };
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -243,7 +247,27 @@ struct Ops {
   static void nz(const uint32_t* v, int64_t n, int* f, cudaStream_t s) {
     if (n) nonzero_kernel<L><<<blocks_for(n, 256), 256, 0, s>>>(v, n, f);
   }
-  static LOps make() { return LOps{pass, split, split_occupancy, shortp, wide, l2s, s2l, mont, zero, dproj, tctx, tcltile, tclapply, tcproj, addm, rrows, lcomb, nz}; }
+  static bool passmk(int first, int64_t nslices, cudaStream_t s, const SpmvArgs& a, const ModParams& mp) {
+    if constexpr (L <= 8) {
+      const unsigned grid = blocks_for(nslices * 32, 256);
+      if (!grid) return true;
+      if (first) spmv_pass<L, 1, true, true, true><<<grid, 256, 0, s>>>(a, mp);
+      else spmv_pass<L, 1, false, true, true><<<grid, 256, 0, s>>>(a, mp);
+      return true;
+    }
+    return false;
+  }
+  static bool mkgather(const uint32_t* y, const int32_t* slot_row, int64_t nslots, uint32_t* out, cudaStream_t s) {
+    if constexpr (L <= 8) {
+      if (nslots) mk_slot_gather<L><<<blocks_for(nslots, 256), 256, 0, s>>>(y, slot_row, nslots, out);
+      return true;
+    }
+    return false;
+  }
+  static LOps make() {
+    return LOps{pass, split, split_occupancy, shortp, wide, l2s, s2l, mont, zero, dproj, tctx, tcltile, tclapply,
+                tcproj, addm, rrows, lcomb, nz, passmk, mkgather};
+  }
 };
 
 template <int L, int LMIN>

@@ -377,6 +377,30 @@ class DeviceMatrix:
     def spmv(self, vin: DeviceVector, vout: DeviceVector):
         N.check(N.load().sld_spmv(self._h, vin.handle, vout.handle))
 
+    def mksol_bind(self, ys) -> bool:
+        """Bind n <= 8 y vectors for `spmv_mksol` (slot-order copies on the
+        device).  False when this layout cannot fuse the step (short rows,
+        limb slicing, die split, several chains, l >= 2^256)."""
+        lib = N.load()
+        if not ys:
+            N.check(lib.sld_mat_mksol_bind(self._h, None, 0))
+            return False
+        if self.L > 8 or self.chains != 1 or len(ys) > 8:
+            return False
+        info = self.info()
+        if info["rows_per_slice"] != 32 or info["lanes_per_residue"] != 1 or info["halves"] != 1:
+            return False  # short rows / limb slicing / die split
+        arr = (ctypes.c_void_p * len(ys))(*[y.handle.value if hasattr(y.handle, "value") else y.handle
+                                            for y in ys])
+        N.check(lib.sld_mat_mksol_bind(self._h, arr, len(ys)))
+        return True
+
+    def spmv_mksol(self, vin: DeviceVector, vout: DeviceVector, coeffs):
+        """vout = A vin + sum_s coeffs[s] y_s mod l (the bound y vectors),
+        one product with the combination in its epilogue; asynchronous."""
+        cl = ints_to_limbs([int(c) for c in coeffs], self.L)
+        N.check(N.load().sld_spmv_mksol(self._h, vin.handle, vout.handle, N.ptr(cl)))
+
     def krylov_unit(self, v: DeviceVector, rows, steps):
         """terms (steps, m, L) -- or (steps, chains, m, L) for several chains."""
         rows = N.c64(rows)

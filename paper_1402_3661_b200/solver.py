@@ -251,12 +251,21 @@ class B200Multiplier:
                     lincomb(dm.field, [y for y, _ in part], [c for _, c in part], dst,
                             acc if k0 == 0 else dst)
 
+            # the Horner step in one product when the layout allows: the
+            # combination runs in the SpMV's last-pass epilogue
+            fused = dmax > 0 and os.environ.get("SLD_MKSOL_FUSED", "1") != "0" and dm.mksol_bind(ys)
             combo(dmax, None, w)
             horner = 0
             for i in range(dmax - 1, -1, -1):
-                dm.spmv(w, t)
+                if fused:
+                    dm.spmv_mksol(w, t, [p[i] if i <= _poly_degree(p) else 0 for p in G])
+                    w, t = t, w
+                else:
+                    dm.spmv(w, t)
+                    combo(i, t, w)
                 horner += 1
-                combo(i, t, w)
+            if fused:
+                dm.mksol_bind([])
             tail = 0
             dm.spmv(w, t)
             while t.nonzero() and tail < val:

@@ -163,3 +163,71 @@ def test_tensor_core_combination_vs_python(bits, n, extreme):
         want = [(a + sum(c * y[i] for c, y in zip(cs, ys))) % ell for i, a in enumerate(base)]
         assert got == want, trial
     lc.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fused", "unfused"])
+def test_device_mksol_fused_step_matches_reference(monkeypatch, mode):
+    # the Horner step as ONE product (combination in the last pass's
+    # epilogue, sld_spmv_mksol) and as SpMV + combination kernel: both give
+    # the reference's kernel vectors.  SLD_SHORT=0 keeps these small
+    # matrices on the pass layout the fused step runs on.
+    from paper_1402_3661_b200.device import DeviceMatrix
+    monkeypatch.setenv("SLD_SHORT", "0")
+    monkeypatch.setenv("SLD_MKSOL_FUSED", "1" if mode == "fused" else "0")
+    calls = []
+    orig = DeviceMatrix.spmv_mksol
+    monkeypatch.setattr(DeviceMatrix, "spmv_mksol", lambda self, *a: (calls.append(1), orig(self, *a)))
+    for A, Y, polys, w, (horner, tail, ver) in _cases():
+        mul = B200Multiplier(A)
+        kv = mksol_block(A, Y, type("G", (), {"polys": polys})(), mul=mul)
+        assert kv.w == w
+        assert (kv.horner_spmvs, kv.tail_spmvs, kv.verified) == (horner, tail, True)
+    assert (len(calls) > 0) == (mode == "fused")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [31, 64, 160, 202, 256])
+@pytest.mark.parametrize("n,extreme", [(1, False), (3, False), (8, False), (8, True)])
+@pytest.mark.parametrize("stripes", [1, 3])
+def test_spmv_mksol_vs_python(monkeypatch, bits, n, extreme, stripes):
+    # out = A in + sum_s c_s y_s mod l in one product: +-1 / small / full
+    # entries, a dense column, several column stripes (slot-indexed partials
+    # before the fused last pass), padding slots; extreme: every y, c and
+    # input l - 1
+    from helpers import rand_matrix
+    from paper_1402_3661_b200.device import DeviceMatrix, DeviceVector
+    from paper_1402_3661_b200.modring import next_prime
+    monkeypatch.setenv("SLD_SHORT", "0")
+    ell = next_prime((1 << bits) - (1 << (bits // 2)))
+    if ell.bit_length() > bits:
+        ell = next_prime(1 << (bits - 1))
+    mod = PrimeModulus(ell)
+    rng = np.random.default_rng(bits * 7 + n + stripes)
+    nr = 1000
+    A = rand_matrix(mod, rng, nr, nr - 1, 14, dense=1)
+    dm = DeviceMatrix(A, stripe_cols=(A.total_cols + stripes - 1) // stripes if stripes > 1 else 0)
+    assert dm.info()["stripes"] == stripes
+    f = dm.field
+    ys = [[ell - 1] * nr if extreme else mod.random_residues(rng, nr) for _ in range(n)]
+    u = [ell - 1] * A.total_cols if extreme else mod.random_residues(rng, A.total_cols)
+    dys = []
+    for y in ys:
+        d = DeviceVector(f, A.total_cols)
+        d.upload_limbs(ints_to_limbs(y + [0] * (A.total_cols - nr), mod.limbs))
+        dys.append(d)
+    assert dm.mksol_bind(dys)
+    vin, vout = dm.vector(), dm.vector()
+    vin.upload_limbs(ints_to_limbs(u, mod.limbs))
+    Au = O.limbs_to_ints(to_oracle(A).spmv_limbs(O.ints_to_limbs(u, mod.limbs)))
+    for trial in range(3):
+        cs = [ell - 1] * n if extreme else mod.random_residues(rng, n)
+        if trial == 1:
+            cs[0] = 0
+        dm.spmv_mksol(vin, vout, cs)
+        got = limbs_to_ints(vout.download_limbs())[:nr]
+        want = [(Au[i] + sum(c * y[i] for c, y in zip(cs, ys))) % ell for i in range(nr)]
+        assert got == want, trial
+    dm.mksol_bind([])
+    with pytest.raises(ValueError):
+        dm.spmv_mksol(vin, vout, cs)  # unbound

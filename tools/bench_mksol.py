@@ -38,19 +38,23 @@ def main():
     _, spmv = dm.bench(v, 64, 0)
     mul.mksol(Y, [p[:3] for p in polys])  # warm-up (allocations, module load)
     # the per-step cost is the slope between two degrees (the y uploads and
-    # the set-up of each call cancel)
-    res = []
-    for deg in (a.degree // 4, a.degree):
-        best = None
-        for _ in range(3):  # best of 3: clocks and host jitter
-            t = time.perf_counter()
-            w, verified, horner, tail = mul.mksol(Y, [p[:deg + 1] for p in polys])
-            dt = time.perf_counter() - t
-            best = dt if best is None else min(best, dt)
-        res.append((horner, best))
-    (h0, t0), (h1, t1) = res
-    print(f"{a.config} mksol n={a.n}: {h1} Horner steps in {t1:.3f} s, {h0} in {t0:.3f} s -> "
-          f"{(t1 - t0) / (h1 - h0) * 1e3:.3f} ms per Horner step; plain SpMV {spmv:.3f} ms")
+    # the set-up of each call cancel); the fused step (combination in the
+    # SpMV epilogue) against SpMV + combination kernel
+    for fused in ("1", "0"):
+        os.environ["SLD_MKSOL_FUSED"] = fused
+        res = []
+        for deg in (a.degree // 4, a.degree):
+            best = None
+            for _ in range(3):  # best of 3: clocks and host jitter
+                t = time.perf_counter()
+                w, verified, horner, tail = mul.mksol(Y, [p[:deg + 1] for p in polys])
+                dt = time.perf_counter() - t
+                best = dt if best is None else min(best, dt)
+            res.append((horner, best))
+        (h0, t0), (h1, t1) = res
+        print(f"{a.config} mksol n={a.n} {'fused' if fused == '1' else 'two kernels'}: {h1} Horner steps in "
+              f"{t1:.3f} s, {h0} in {t0:.3f} s -> {(t1 - t0) / (h1 - h0) * 1e3:.3f} ms per Horner step; "
+              f"plain SpMV {spmv:.3f} ms", flush=True)
 
 
 if __name__ == "__main__":
