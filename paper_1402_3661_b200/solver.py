@@ -251,9 +251,11 @@ class B200Multiplier:
                     lincomb(dm.field, [y for y, _ in part], [c for _, c in part], dst,
                             acc if k0 == 0 else dst)
 
-            # the Horner step in one product when the layout allows: the
-            # combination runs in the SpMV's last-pass epilogue
-            fused = dmax > 0 and os.environ.get("SLD_MKSOL_FUSED", "1") != "0" and dm.mksol_bind(ys)
+            # SLD_MKSOL_FUSED=1: the Horner step as one product, the
+            # combination in the SpMV's last-pass epilogue (pass layouts).
+            # Measured level with the tensor-core combination kernel (cfg3
+            # 1.91 vs 1.87 ms, cfg2 0.323 vs 0.335 ms), so it is opt-in.
+            fused = dmax > 0 and os.environ.get("SLD_MKSOL_FUSED", "0") == "1" and dm.mksol_bind(ys)
             combo(dmax, None, w)
             horner = 0
             for i in range(dmax - 1, -1, -1):

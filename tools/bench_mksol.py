@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--n", type=int, default=8)
     ap.add_argument("--degree", type=int, default=48)
+    ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
@@ -40,12 +41,14 @@ def main():
     # the per-step cost is the slope between two degrees (the y uploads and
     # the set-up of each call cancel); the fused step (combination in the
     # SpMV epilogue) against SpMV + combination kernel
+    ws = []
     for fused in ("1", "0"):
         os.environ["SLD_MKSOL_FUSED"] = fused
+        ws.append(mul.mksol(Y, [p[:a.degree + 1] for p in polys])[0])
         res = []
         for deg in (a.degree // 4, a.degree):
             best = None
-            for _ in range(3):  # best of 3: clocks and host jitter
+            for _ in range(a.reps):  # best of reps: clocks and host jitter
                 t = time.perf_counter()
                 w, verified, horner, tail = mul.mksol(Y, [p[:deg + 1] for p in polys])
                 dt = time.perf_counter() - t
@@ -55,6 +58,7 @@ def main():
         print(f"{a.config} mksol n={a.n} {'fused' if fused == '1' else 'two kernels'}: {h1} Horner steps in "
               f"{t1:.3f} s, {h0} in {t0:.3f} s -> {(t1 - t0) / (h1 - h0) * 1e3:.3f} ms per Horner step; "
               f"plain SpMV {spmv:.3f} ms", flush=True)
+    print(f"fused and two-kernel Horner results identical: {all(np.array_equal(ws[0], x) for x in ws[1:])}")
 
 
 if __name__ == "__main__":
