@@ -28,6 +28,10 @@ for tc in 1 0; do SLD_DENSE_TC=$tc timeout 300 python tools/bench_dense.py --con
   > $O/dense_cfg3_tc${tc}_$TAG.txt 2>/dev/null; done
 timeout 600 ncu --set full --graph-profiling node --clock-control none -k regex:tc_digit_gemm -s 2 -c 1 \
   -o $O/full_tcgemm_$TAG python tools/bench_dense.py --config cfg3 --m 16 --steps 4 > /dev/null 2>&1
+# Mksol: Horner step timing (fused vs two kernels) and the tensor-core combination kernel
+timeout 900 python tools/bench_mksol.py --config cfg3 --n 8 --degree 800 --reps 5 > $O/mksol_cfg3_$TAG.txt 2>/dev/null
+timeout 600 ncu --set full --clock-control none -k regex:tcl_combine -s 4 -c 1 \
+  -o $O/full_tcl_$TAG python tools/bench_mksol.py --config cfg3 --n 8 --degree 8 --reps 1 > /dev/null 2>&1
 # DRAM bytes per step of the benched layouts (bench.py reads profiles/traffic_*.json)
 python tools/traffic_from_launches.py $O/launches_cfg3_$TAG.csv cfg3 2 4 $O/traffic_cfg3_g2_$TAG.json "spmv_pass<7, 2," > /dev/null
 python tools/traffic_from_launches.py $O/launches_cfg2_$TAG.csv cfg2 1 1 $O/traffic_cfg2_g1_$TAG.json > /dev/null
