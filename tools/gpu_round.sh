@@ -36,4 +36,10 @@ timeout 600 ncu --set full --clock-control none -k regex:tcl_combine -s 4 -c 1 \
 python tools/traffic_from_launches.py $O/launches_cfg3_$TAG.csv cfg3 2 4 $O/traffic_cfg3_g2_$TAG.json "spmv_pass<7, 2," > /dev/null
 python tools/traffic_from_launches.py $O/launches_cfg2_$TAG.csv cfg2 1 1 $O/traffic_cfg2_g1_$TAG.json > /dev/null
 python tools/traffic_from_launches.py $O/launches_cfg5_$TAG.csv cfg5 1 1 $O/traffic_cfg5_g1_$TAG.json > /dev/null
+# summaries of the full captures; only the SpMV report travels back (gpurun
+# copies at most 64 MiB of gpurun_out/)
+for r in $O/full_cfg3_$TAG $O/full_tcgemm_$TAG $O/full_tcl_$TAG; do
+  [ -f $r.ncu-rep ] && python tools/ncu_summary.py $r.ncu-rep $r.json > /dev/null 2>&1
+done
+rm -f $O/full_tcgemm_$TAG.ncu-rep $O/full_tcl_$TAG.ncu-rep
 tail -2 $O/gputests_$TAG.log; tail -1 $O/smoke_$TAG.log
