@@ -176,6 +176,9 @@ int sld_vec_read_rows(sld_vec *v, const int64_t *rows, int m, uint32_t *limbs);
  * have total_cols residues and `out` nrows residues (and be distinct).
  */
 int sld_spmv(sld_mat *m, sld_vec *in, sld_vec *out);
+/* sld_spmv without the final stream synchronize (errors surface at the next
+ * synchronizing call). */
+int sld_spmv_async(sld_mat *m, sld_vec *in, sld_vec *out);
 
 /* Host-buffer convenience: planes in, planes out (the multiplier's
  * `.apply(planes)` contract, solver.py:140-142). */

@@ -35,7 +35,7 @@ EXPORTS = [
     "sld_lcset_create", "sld_lcset_apply", "sld_lcset_destroy",
     "sld_mat_set_peers", "sld_spmv_peers", "sld_peer_barrier", "sld_memcpy_async", "sld_dev_alloc", "sld_dev_free",
     "sld_ipc_get", "sld_ipc_open", "sld_ipc_close",
-    "sld_spmv", "sld_spmv_planes", "sld_krylov_unit",
+    "sld_spmv", "sld_spmv_async", "sld_spmv_planes", "sld_krylov_unit",
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
     "sld_bench_spmv", "sld_corpus_rows", "sld_corpus_fill",
     "sld_sldm_info", "sld_sldm_read", "sld_sldm_write", "sld_sldv_write", "sld_sldv_info", "sld_sldv_read",
@@ -112,6 +112,7 @@ def load(build_if_missing=False):
             "sld_vec_download_limbs": ([vp, vp, i64], i32),
             "sld_vec_device_ptr": ([vp, vp, vp], i32),
             "sld_spmv": ([vp, vp, vp], i32),
+            "sld_spmv_async": ([vp, vp, vp], i32),
             "sld_spmv_planes": ([vp, vp, vp, i32], i32),
             "sld_krylov_unit": ([vp, vp, vp, i32, i64, vp], i32),
             "sld_xblock_create": ([vp, vp, i32, i64, pp], i32),

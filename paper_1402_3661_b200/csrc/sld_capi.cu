@@ -1482,7 +1482,15 @@ static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int
   }
 }
 
-extern "C" int sld_spmv(sld_mat* M, sld_vec* in, sld_vec* out) {
+static int spmv_checked(sld_mat* M, sld_vec* in, sld_vec* out, bool sync);
+
+extern "C" int sld_spmv(sld_mat* M, sld_vec* in, sld_vec* out) { return spmv_checked(M, in, out, true); }
+
+// the same product left in flight on the context stream (Horner loops that
+// enqueue the next kernel without a host round trip)
+extern "C" int sld_spmv_async(sld_mat* M, sld_vec* in, sld_vec* out) { return spmv_checked(M, in, out, false); }
+
+static int spmv_checked(sld_mat* M, sld_vec* in, sld_vec* out, bool sync) {
   if (!M || !in || !out) return fail(SLD_E_ARG, "null argument");
   if (in->n != M->total_cols) return fail(SLD_E_ARG, "vector length %lld != %lld columns",
                                           (long long)in->n, (long long)M->total_cols);
@@ -1494,7 +1502,7 @@ extern "C" int sld_spmv(sld_mat* M, sld_vec* in, sld_vec* out) {
   CU(cudaSetDevice(M->ctx->dev));
   launch_product(M, in->buf[in->cur], out->buf[out->cur], nullptr, 0, nullptr);
   CU(cudaGetLastError());
-  CU(cudaStreamSynchronize(M->ctx->stream));
+  if (sync) CU(cudaStreamSynchronize(M->ctx->stream));
   return SLD_OK;
 }
 

@@ -374,8 +374,9 @@ class DeviceMatrix:
         N.check(N.load().sld_spmv_planes(self._h, N.ptr(p), N.ptr(out), p.shape[-1]))
         return out
 
-    def spmv(self, vin: DeviceVector, vout: DeviceVector):
-        N.check(N.load().sld_spmv(self._h, vin.handle, vout.handle))
+    def spmv(self, vin: DeviceVector, vout: DeviceVector, sync=True):
+        lib = N.load()
+        N.check((lib.sld_spmv if sync else lib.sld_spmv_async)(self._h, vin.handle, vout.handle))
 
     def mksol_bind(self, ys) -> bool:
         """Bind n <= 8 y vectors for `spmv_mksol` (slot-order copies on the

@@ -263,7 +263,7 @@ class B200Multiplier:
                     dm.spmv_mksol(w, t, [p[i] if i <= _poly_degree(p) else 0 for p in G])
                     w, t = t, w
                 else:
-                    dm.spmv(w, t)
+                    dm.spmv(w, t, sync=False)  # in stream order with the combination
                     combo(i, t, w)
                 horner += 1
             if fused:
