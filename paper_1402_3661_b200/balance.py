@@ -187,7 +187,8 @@ def _block(A, p: PermutationPair, n_pad: int, r: int, c: int, i: int, j: int, ex
         N.check(int(nb))
     src = np.empty(nb, dtype=np.int64)
     lc = np.empty(nb, dtype=np.int32)
-    N.check(int(min(0, lib.sld_split_block(*args, N.ptr(src), N.ptr(lc), 0))))
+    if nb:
+        N.check(int(min(0, lib.sld_split_block(*args, N.ptr(src), N.ptr(lc), 0))))
     nnz = len(A.col_idx)
     inner = src < nnz
     tags = np.empty(nb, dtype=np.uint8)

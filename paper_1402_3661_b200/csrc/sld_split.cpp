@@ -69,7 +69,7 @@ extern "C" int64_t sld_split_block(int64_t nrows, const int64_t* row_ptr, const 
                                    int32_t threads) {
   if (nrows < 0 || n_pad < nrows || r < 1 || c < 1 || n_pad % r || n_pad % c || bi < 0 || bi >= r || bj < 0 ||
       bj >= c || (col_bytes != 4 && col_bytes != 8) || n_extra < 0 || !rp || (nrows && (!row_ptr || !row_perm)) ||
-      (n_extra && (!extra_r || !extra_c)) || !col_perm || (src && !lc))
+      (n_extra && (!extra_r || !extra_c)) || (n_pad && !col_perm) || (src && !lc))
     return sld_set_error(SLD_E_INVAL, "sld_split_block: bad arguments");
   Split s{nrows, n_pad, n_pad / r, n_pad / c, row_ptr, col_idx, col_bytes, row_perm, col_perm,
           n_extra, extra_r, extra_c, bi, bj};

@@ -104,3 +104,19 @@ def test_bad_permutation_raises():
         split(A, p, g)
     with pytest.raises(ValueError):
         split(A, identity_permutation(A, GridSpec(3, 1)), g)  # 21 != 20 rows
+
+
+@pytest.mark.parametrize("rows", [[], [[(0, 5)]], [[], []]])
+@pytest.mark.parametrize("grid", [(1, 1), (2, 2), (2, 3)])
+def test_empty_and_tiny_matrices(rows, grid):
+    mod = PrimeModulus(2**61 - 1)
+    n = len(rows)
+    A = SparseMatrix.from_rows(mod, n, n, rows)
+    g = GridSpec(*grid)
+    p = balance_permutation(A, g)
+    want = lexsort_split(A, p, g)
+    bs = split(A, p, g)
+    for i in range(g.r):
+        for j in range(g.c):
+            same_block(bs.blocks[i][j], want.get((i, j), (np.zeros(bs.block_rows + 1, np.int64), [], [], [], {})))
+    assert permuted_padded(A, p, g).nrows == padded_size(n, g)
