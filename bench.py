@@ -356,10 +356,10 @@ def max_over_ranks(dist, x, local):
     return float(t.item())
 
 
-def config_block(name, cfg, A, mod, world):
+def config_block(name, cfg, A, mod, world, chains=1):
     return {"workload": f"{name}: {cfg['desc']}", "N": A.nrows, "nnz": int(len(A.col_idx)),
             "ell_bits": mod.bit_length, "gamma": cfg["gamma"], "bp": list(cfg["bp"]),
-            "parallelism": f"independent Krylov chains, 1 per GPU x {world}",
+            "parallelism": f"independent Krylov chains, {chains} per GPU x {world} GPU(s)",
             "l2": "inputs larger than L2 (matrix streams >1 GB/step at cfg3); the iterate vector's "
                   "reuse across steps is the Krylov recurrence itself"}
 
@@ -560,7 +560,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 limbs, exact mod l (int64 lazy accumulation)",
         "data": "synthetic (native corpus generator, FFS profile, seed 1, planted kernel column)",
-        "config": dict(config_block(args.config, cfg, A, mod, world), chains_per_gpu=G,
+        "config": dict(config_block(args.config, cfg, A, mod, world, chains=G), chains_per_gpu=G,
                        step=f"one product of each of the {G} chain(s) on every GPU",
                        sequences=(f"{G} of the block-Wiedemann sequences per GPU share each matrix pass "
                                   f"(chain group); one_chain_per_gpu times one sequence per GPU"
