@@ -210,19 +210,25 @@ def _block(A, p: PermutationPair, n_pad: int, r: int, c: int, i: int, j: int, ex
 
 
 class BlockSplit:
-    """r x c blocks (local indices) of the permuted, padded matrix."""
+    """r x c blocks (local indices) of the permuted, padded matrix plus the
+    pinned rows (balance.py:181-198)."""
 
-    def __init__(self, blocks, grid: GridSpec, n_original: int, n_padded: int):
+    def __init__(self, blocks, grid: GridSpec, n_original: int, n_padded: int, pin_rows=None):
         self.blocks = blocks
         self.grid = grid
         self.n_original = n_original
         self.n_padded = n_padded
+        # one pinned +1 entry (i, i) per padded coordinate (balance.py:210)
+        self.pin_rows = list(pin_rows) if pin_rows is not None else \
+            [(i, i) for i in range(n_original, n_padded)]
         self.block_rows = n_padded // grid.r
         self.block_cols = n_padded // grid.c
 
     @property
     def pad_rows(self) -> int:
         return self.n_padded - self.n_original
+
+    pad_cols = pad_rows
 
 
 def split(A, p: PermutationPair, g: GridSpec, only=None) -> BlockSplit:

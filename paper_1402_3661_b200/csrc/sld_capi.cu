@@ -135,9 +135,29 @@ struct sld_ctx {
   uint32_t* coef = nullptr;    // lincomb coefficient staging (64 x SW words)
   uint8_t* die_map = nullptr;  // device copy of the %smid -> die map (256 entries)
   int die_n[2] = {0, 0};       // SMs per die; both 0 if the map is unavailable
+  // lifetime: the owner's handle plus one reference per vector / matrix /
+  // projection block / combination set made on this context, so handles may
+  // be destroyed in any order (a garbage collector frees them in arbitrary
+  // order) without touching a freed context
+  std::atomic<int> refs{1};
+};
+
+static void ctx_free(sld_ctx* c);
+static void ctx_unref(sld_ctx* c) {
+  if (c && c->refs.fetch_sub(1) == 1) ctx_free(c);
+}
+// a context reference held by an object made on it (released on delete)
+struct CtxRef {
+  sld_ctx* c = nullptr;
+  void bind(sld_ctx* x) {
+    c = x;
+    if (c) c->refs.fetch_add(1);
+  }
+  ~CtxRef() { ctx_unref(c); }
 };
 
 struct sld_vec {
+  CtxRef ref;
   sld_ctx* ctx = nullptr;
   int64_t n = 0;      // residues per chain
   int chains = 1;     // G chains interleaved per record (row*G + chain)
@@ -146,6 +166,7 @@ struct sld_vec {
 };
 
 struct sld_xblock {
+  CtxRef ref;
   sld_ctx* ctx = nullptr;
   int m = 0;
   int64_t n = 0;
@@ -162,6 +183,7 @@ struct sld_xblock {
 };
 
 struct sld_mat {
+  CtxRef ref;
   sld_ctx* ctx = nullptr;
   int64_t nrows = 0, ncols = 0, total_cols = 0, nnz = 0;
   int n_dense = 0;
@@ -519,7 +541,11 @@ extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_
 }
 
 extern "C" int sld_ctx_destroy(sld_ctx* c) {
-  if (!c) return SLD_OK;
+  ctx_unref(c);  // freed once the last object made on it is destroyed too
+  return SLD_OK;
+}
+
+static void ctx_free(sld_ctx* c) {
   cudaSetDevice(c->dev);
   if (c->own) cudaStreamDestroy(c->own);
   if (c->die_map) cudaFree(c->die_map);
@@ -528,7 +554,6 @@ extern "C" int sld_ctx_destroy(sld_ctx* c) {
   if (c->hstage) cudaFreeHost(c->hstage);
   if (c->dstage) cudaFree(c->dstage);
   delete c;
-  return SLD_OK;
 }
 
 extern "C" int sld_ctx_sync(sld_ctx* c) {
@@ -579,6 +604,7 @@ extern "C" int sld_vec_create_chains(sld_ctx* ctx, int64_t n, int chains, sld_ve
   CU(cudaSetDevice(ctx->dev));
   auto v = std::make_unique<sld_vec>();
   v->ctx = ctx;
+  v->ref.bind(ctx);
   v->n = n;
   v->chains = chains;
   TRY(vec_alloc_buf(v.get(), 0));
@@ -815,6 +841,7 @@ extern "C" int sld_lincomb(sld_ctx* c, const uint64_t* y_ptrs, const uint32_t* c
 // (the y block) tiled once as byte digits; per Horner step one launch
 // combines them with the step's coefficients and adds acc (sld_tcgemm.cuh)
 struct sld_lcset {
+  CtxRef ref;
   sld_ctx* ctx = nullptr;
   int n = 0;
   int64_t rows = 0, mtiles = 0;
@@ -828,6 +855,7 @@ extern "C" int sld_lcset_create(sld_ctx* c, const uint64_t* y_ptrs, int n, int64
   CU(cudaSetDevice(c->dev));
   auto S = std::make_unique<sld_lcset>();
   S->ctx = c;
+  S->ref.bind(c);
   S->n = n;
   S->rows = rows;
   S->mtiles = (rows + 127) / 128;
@@ -1341,6 +1369,7 @@ extern "C" int sld_mat_create_chains(sld_ctx* ctx, int chains, int64_t nrows, in
   CU(cudaSetDevice(ctx->dev));
   sld_mat* M = new sld_mat();
   M->ctx = ctx;
+  M->ref.bind(ctx);
   M->chains = chains;
   M->nrows = nrows;
   M->ncols = ncols;
@@ -1810,6 +1839,7 @@ extern "C" int sld_xblock_create(sld_ctx* ctx, const uint32_t* x_limbs, int m, i
   CU(cudaSetDevice(ctx->dev));
   auto xb = std::make_unique<sld_xblock>();
   xb->ctx = ctx;
+  xb->ref.bind(ctx);
   xb->m = m;
   xb->n = n;
   const size_t cnt = (size_t)m * n;
@@ -1849,6 +1879,9 @@ extern "C" int sld_xblock_create(sld_ctx* ctx, const uint32_t* x_limbs, int m, i
       xb->ktiles = (n + TC_BK - 1) / TC_BK;
       const int64_t max_kt = TC_MAX_K_PER_CTA / TC_BK;
       xb->nct = (int)std::max<int64_t>(ctx->sms, (xb->ktiles + max_kt - 1) / max_kt);
+      // test hook: the fewest CTAs the accumulator bound allows, so each
+      // CTA sums the maximum K (tests/test_krylov_gpu.py exactness at the cap)
+      if (const char* e = getenv("SLD_TC_MAX_K")) if (atoi(e)) xb->nct = (int)((xb->ktiles + max_kt - 1) / max_kt);
       xb->kt_per_cta = (xb->ktiles + xb->nct - 1) / xb->nct;
       xb->nct = (int)((xb->ktiles + xb->kt_per_cta - 1) / xb->kt_per_cta);
       CU(cudaMalloc(&xb->A, (size_t)xb->ktiles * xb->MT * TC_MTILE_BYTES));

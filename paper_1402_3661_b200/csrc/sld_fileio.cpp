@@ -101,22 +101,37 @@ struct Cur {
 
 // ell header: u16 byte width, ell big-endian
 struct Ell {
-  int eb = 0, L = 0;
+  int hb = 0;  // bytes of the modulus field in the header
+  int eb = 0;  // residue width: the modulus's minimal byte width (PrimeModulus.byte_width)
+  int L = 0;
   std::vector<uint32_t> w;  // little-endian limbs
 };
 
 int read_ell(Cur& c, Ell* e, uint8_t* ell_be, int cap) {
-  uint16_t eb;
-  TRYF(c.get(&eb));
+  uint16_t hb;
+  TRYF(c.get(&hb));
   const uint8_t* q;
-  TRYF(c.take(eb, &q));
-  if (eb == 0 || eb > 129) return ferr(SLD_E_FORMAT, "%s: modulus byte width %d out of range", c.name, eb);
-  if (ell_be && cap >= eb) memcpy(ell_be, q, eb);
-  e->eb = eb;
-  e->L = (eb + 3) / 4;
+  TRYF(c.take(hb, &q));
+  if (hb == 0) return ferr(SLD_E_FORMAT, "%s: empty modulus field", c.name);
+  if (ell_be) {
+    if (cap < hb) return ferr(SLD_E_FORMAT, "%s: modulus field of %d bytes exceeds %d", c.name, hb, cap);
+    memcpy(ell_be, q, hb);
+  }
+  e->hb = hb;
+  e->L = (hb + 3) / 4;
   e->w.assign(e->L + 1, 0);
-  for (int i = 0; i < eb; i++) e->w[i / 4] |= (uint32_t)q[eb - 1 - i] << (8 * (i % 4));
+  for (int i = 0; i < hb; i++) e->w[i / 4] |= (uint32_t)q[hb - 1 - i] << (8 * (i % 4));
   while (e->L > 1 && e->w[e->L - 1] == 0) e->L--;
+  // residues are written at the modulus's own byte width, whatever zero
+  // padding the header field carries (spmatrix.py:345-352, modring.py:112-130)
+  int bits = 0;
+  for (int i = e->L - 1; i >= 0; i--)
+    if (e->w[i]) {
+      bits = 32 * i + 32 - __builtin_clz(e->w[i]);
+      break;
+    }
+  if (bits < 2 || bits > 1024) return ferr(SLD_E_FORMAT, "%s: modulus of %d bits out of range", c.name, bits);
+  e->eb = (bits + 7) / 8;
   return SLD_OK;
 }
 
@@ -543,7 +558,7 @@ extern "C" int sld_sldm_info(const char* path, int header_only, int64_t* info, u
     memset(info, 0, 8 * sizeof(int64_t));
     info[0] = (int64_t)nr;
     info[1] = (int64_t)nc;
-    info[2] = h.ell.eb;
+    info[2] = h.ell.hb;
     info[7] = h.ell.L;
     return SLD_OK;
   }
@@ -555,7 +570,7 @@ extern "C" int sld_sldm_info(const char* path, int header_only, int64_t* info, u
   TRYF(c.done());
   info[0] = h.nrows;
   info[1] = h.ncols;
-  info[2] = h.ell.eb;
+  info[2] = h.ell.hb;
   info[3] = (int64_t)h.dense_idx.size();
   info[4] = nnz;
   info[5] = nf;
@@ -743,7 +758,7 @@ extern "C" int sld_sldv_info(const char* path, int header_only, int64_t* info, u
   if (header_only) {
     memset(info, 0, 6 * sizeof(int64_t));
     info[0] = kind;
-    info[1] = e.eb;
+    info[1] = e.hb;
     info[2] = e.L;
     return SLD_OK;
   }
@@ -754,11 +769,17 @@ extern "C" int sld_sldv_info(const char* path, int header_only, int64_t* info, u
   }
   uint64_t count;
   TRYF(c.get(&count));
+  // count * m * width must fit what is left of the file (no wrap-around)
+  const uint64_t left = (uint64_t)(c.n - c.pos);
+  const uint64_t per = (uint64_t)m * (uint64_t)e.eb;
+  if (per && count > left / per)
+    return ferr(SLD_E_TRUNC, "%s: %llu x %u residues of %d bytes exceed the %llu bytes left", path,
+                (unsigned long long)count, m, e.eb, (unsigned long long)left);
   const uint64_t nres = count * m;
   TRYF(c.take((size_t)nres * e.eb, &q));
   TRYF(c.done());
   info[0] = kind;
-  info[1] = e.eb;
+  info[1] = e.hb;
   info[2] = e.L;
   info[3] = m;
   info[4] = (int64_t)count;

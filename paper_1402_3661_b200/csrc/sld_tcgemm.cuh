@@ -11,8 +11,9 @@
 //   tile(kt) = [mt][ks][mg][kc][8 rows][16 bytes]
 // kt: 128-byte K tile, mt: 128-row M tile, ks: 32-byte UMMA_K step,
 // mg: 8-row group, kc: 16-byte K chunk.  Descriptor: LBO = 128 B (kc),
-// SBO = 256 B (mg).  Split-K: CTA c owns a K range of <= 65536 bytes, so a
-// u8 x u8 sum (< 2^16 per term) never exceeds 2^32 in its s32 accumulator;
+// SBO = 256 B (mg).  Split-K: CTA c owns a K range of <= 32768 bytes, so a
+// u8 x u8 sum (<= 255^2 = 65025 per term) stays below 32768 * 65025 < 2^31:
+// the s32 accumulator never wraps (exactness does not lean on wrap-around);
 // the per-CTA tiles are summed in 64 bits afterwards.
 #pragma once
 #include <cstdint>
@@ -25,7 +26,8 @@ constexpr int TC_STAGES = 3;
 constexpr int TC_MTILE_BYTES = 128 * TC_BK;       // 16 KB
 constexpr int TC_BTILE_BYTES = TC_NQ * TC_BK;     // 4 KB
 constexpr int TC_THREADS = 192;                   // w0 loads, w1 MMA, w2-5 epilogue
-constexpr int64_t TC_MAX_K_PER_CTA = 65536;
+constexpr int64_t TC_MAX_K_PER_CTA = 32768;
+static_assert(TC_MAX_K_PER_CTA * 65025 < (1ll << 31), "s32 TMEM accumulator must not wrap");
 
 __host__ __device__ constexpr int tc_smem_bytes(int MT) {
   return TC_STAGES * (MT * TC_MTILE_BYTES + TC_BTILE_BYTES) + 1024;

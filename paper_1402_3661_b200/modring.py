@@ -64,6 +64,15 @@ def next_prime(n: int) -> int:
     return n
 
 
+def prev_prime(n: int) -> int:
+    n = int(n) - 1
+    while n >= 2 and not is_probable_prime(n):
+        n -= 1
+    if n < 2:
+        raise ValueError("no prime below 2")
+    return n
+
+
 class PrimeModulus:
     """The prime l defining Z/lZ (sldlag/modring.py:44-130)."""
 

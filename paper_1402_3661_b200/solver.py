@@ -166,6 +166,8 @@ class B200Multiplier:
     def dm(self) -> DeviceMatrix:
         if self._dm is None:
             self._dm = DeviceMatrix(self.A, self.device, stripe_cols=self.stripe_cols)
+        elif isinstance(self._dm, _SharedMatrix):
+            self._dm = self._dm.get()
         return self._dm
 
     def apply(self, planes):
@@ -375,8 +377,12 @@ def krylov_column(mul, xblock, y_planes, count, start_terms=None, checkpoint=Non
     else:
         remaining = count - len(terms)
         while remaining > 0:
-            chunk = remaining if checkpoint is None else min(remaining,
-                                                             _steps_until_flush(checkpoint, col_index))
+            if checkpoint is None:
+                chunk = remaining
+            elif hasattr(checkpoint, "reserve_steps"):  # atomic w.r.t. concurrent columns
+                chunk = min(remaining, max(1, int(checkpoint.reserve_steps(col_index, remaining))))
+            else:
+                chunk = min(remaining, _steps_until_flush(checkpoint, col_index))
             new_terms, v = mul.krylov(xblock, v, chunk)
             spmvs += chunk
             remaining -= chunk
@@ -407,13 +413,22 @@ def krylov_block(A, X, Y, count, muls=None, checkpoint=None, contexts=None,
     if chains_per_gpu > 1 and muls is None and checkpoint is None and isinstance(X, UnitRows) \
             and n >= chains_per_gpu:
         return _krylov_block_grouped(A, X, Y, count, chains_per_gpu, contexts)
+    lanes = None  # default multipliers: column j on device j % ndev
     if muls is None:
         from ._native import device_count
-        ndev = max(1, device_count())
-        muls = [B200Multiplier(A, device=j % ndev) for j in range(n)]
+        ndev = max(1, min(n, device_count()))
+        # one device matrix per GPU shared by the columns placed on it; the
+        # columns of one GPU run one after another on that GPU's host thread
+        # (a DeviceMatrix, like an sld_ctx, is not shared across threads)
+        shared = [_SharedMatrix(A, d) for d in range(ndev)]
+        muls = [B200Multiplier(A, device=j % ndev, dm=shared[j % ndev]) for j in range(n)]
+        lanes = [list(range(d, n, ndev)) for d in range(ndev)]
     mod = muls[0].mod
     if contexts is None:
-        contexts = int(os.environ.get("SLDLAG_CONTEXTS", str(n)))
+        # the reference's default is one context (solver.py:232-233); the
+        # default multipliers get one host thread per GPU
+        env = os.environ.get("SLDLAG_CONTEXTS")
+        contexts = int(env) if env else (len(lanes) if lanes is not None else 1)
 
     def run(j):
         start = checkpoint.load_column(j) if checkpoint is not None else None
@@ -427,14 +442,39 @@ def krylov_block(A, X, Y, count, muls=None, checkpoint=None, contexts=None,
                                         checkpoint=checkpoint, col_index=j)
         return terms, spmvs
 
-    if contexts > 1 and n > 1:
+    results = [None] * n
+    if lanes is not None and contexts > 1 and len(lanes) > 1:
+        def run_lane(cols):
+            for j in cols:
+                results[j] = run(j)
+        with ThreadPoolExecutor(max_workers=min(contexts, len(lanes))) as pool:
+            list(pool.map(run_lane, lanes))
+    elif lanes is None and contexts > 1 and n > 1:
         with ThreadPoolExecutor(max_workers=contexts) as pool:
             results = list(pool.map(run, range(n)))
     else:
         results = [run(j) for j in range(n)]
+    if checkpoint is not None and hasattr(checkpoint, "wait"):
+        checkpoint.wait()  # the final async flushes are durable (and their errors raised)
     m = len(results[0][0][0]) if results and results[0][0] else 0
     return BlockSequence(m=m, n=n, columns=[r[0] for r in results],
                          spmvs_per_column=[r[1] for r in results])
+
+
+class _SharedMatrix:
+    """A DeviceMatrix of A on one device, built on first use and shared by
+    the default multipliers of the columns placed on that device."""
+
+    def __init__(self, A, device):
+        self.A, self.device = A, device
+        self._dm = None
+        self._lock = threading.Lock()
+
+    def get(self) -> DeviceMatrix:
+        with self._lock:
+            if self._dm is None:
+                self._dm = DeviceMatrix(self.A, self.device)
+            return self._dm
 
 
 def _krylov_block_grouped(A, X, Y, count, G, contexts):

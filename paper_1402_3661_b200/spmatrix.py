@@ -284,7 +284,7 @@ def load_matrix(path, dense_as_limbs=False):
     from .fileio import check_io
     from .modring import limbs_to_ints
     info = np.zeros(8, dtype=np.int64)
-    ell_be = np.zeros(160, dtype=np.uint8)
+    ell_be = np.zeros(65536, dtype=np.uint8)
     check_io(N.load().sld_sldm_info(_path(path), 1, N.ptr(info), N.ptr(ell_be), len(ell_be)))
     mod = _ell_from_be(ell_be, int(info[2]))
     check_io(N.load().sld_sldm_info(_path(path), 0, N.ptr(info), N.ptr(ell_be), len(ell_be)))
@@ -333,7 +333,7 @@ def _load_residues(path, want_kind):
     from . import _native as N
     from .fileio import BadMagic, check_io
     info = np.zeros(6, dtype=np.int64)
-    ell_be = np.zeros(160, dtype=np.uint8)
+    ell_be = np.zeros(65536, dtype=np.uint8)
     check_io(N.load().sld_sldv_info(_path(path), 1, N.ptr(info), N.ptr(ell_be), len(ell_be)))
     if int(info[0]) != want_kind:
         raise BadMagic(f"{path}: magic {'SLDQ' if info[0] else 'SLDV'}, expected "

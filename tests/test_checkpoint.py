@@ -70,3 +70,52 @@ def test_attempt_meta_roundtrip(tmp_path):
         CheckpointManager(tmp_path, MOD).begin_attempt(0, X, Y, bp, 98, "unit")
     ck2.discard_attempt()
     assert CheckpointManager(tmp_path, MOD).attempt == 1
+
+
+class _CountingKrylov:
+    """A `.krylov` multiplier whose iterate encodes how many products it has
+    taken (row 0, digit 0), so a flushed iterate can be matched against the
+    flushed term count."""
+
+    def __init__(self, n=8):
+        self.mod, self.size, self.count = MOD, n, 0
+
+    def krylov(self, xblock, v, steps):
+        import time
+        k = int(np.asarray(v)[0, 0])
+        out = np.array(v, dtype=np.uint64, copy=True)
+        out[0, 0] = k + steps
+        time.sleep(0.002 * steps)  # let the other column's thread interleave
+        self.count += steps
+        return [[k + i] for i in range(steps)], out
+
+
+@pytest.mark.parametrize("halt_after", [5, 10, 17])
+def test_concurrent_columns_halt_on_consistent_iterates(tmp_path, halt_after):
+    # ADVICE r01: with columns on concurrent threads, another column's steps
+    # must not make a device chunk halt mid-replay (terms k, iterate k + r)
+    from paper_1402_3661_b200.solver import krylov_block
+    ck = CheckpointManager(tmp_path, MOD, every=6, halt_after=halt_after)
+    ck.m = 1
+    muls = [_CountingKrylov() for _ in range(3)]
+    with pytest.raises(HaltRequested):
+        krylov_block(None, UnitRows([0]), [[0] * 8] * 3, 40, muls=muls, checkpoint=ck, contexts=3)
+    ck.wait()
+    seen = 0
+    for j in range(3):
+        st = ck.load_column(j)
+        if st is None:
+            continue
+        terms, v = st
+        seen += 1
+        assert int(v[0, 0]) == len(terms), f"column {j}: iterate after {int(v[0, 0])} products, {len(terms)} terms"
+        assert [t[0] for t in terms] == list(range(len(terms)))
+    assert seen >= 1
+
+
+def test_async_writer_error_surfaces_on_next_call(tmp_path):
+    ck = CheckpointManager(tmp_path, MOD, every=3, async_writes=True)
+    ck.m = 2
+    ck._errors.append(OSError("disk full"))  # as the writer thread records it
+    with pytest.raises(OSError):
+        ck.on_step(0, [[1, 2]], ints_to_planes([0] * 4, digit_count(MOD.ell)))

@@ -125,3 +125,37 @@ def test_large_roundtrip_threaded(tmp_path):
     assert B == A
     store_matrix(B, tmp_path / "big2.sldm")
     assert p.read_bytes() == (tmp_path / "big2.sldm").read_bytes()
+
+
+def _sldv_bytes(ell, vals, header_width, count=None):
+    import struct
+    eb = (ell.bit_length() + 7) // 8
+    out = b"SLDV" + struct.pack("<I", 1) + struct.pack("<H", header_width) + ell.to_bytes(header_width, "big")
+    out += struct.pack("<Q", len(vals) if count is None else count)
+    return out + b"".join(int(v).to_bytes(eb, "little") for v in vals)
+
+
+def test_sldv_zero_padded_modulus_header(tmp_path):
+    # residues are read at the modulus's own byte width whatever zero padding
+    # the header's ell field has (spmatrix.py:349-352,450-462)
+    from paper_1402_3661_b200 import load_vector
+    ell = 2**200 - 75
+    vals = [0, 1, ell - 1, 12345678901234567890]
+    for hw in (25, 28, 200):
+        p = tmp_path / f"v{hw}.sldv"
+        p.write_bytes(_sldv_bytes(ell, vals, hw))
+        got, mod = load_vector(p)
+        assert got == vals and mod.ell == ell
+
+
+def test_sldv_count_overflow_is_truncation(tmp_path):
+    from paper_1402_3661_b200 import load_vector
+    from paper_1402_3661_b200.fileio import TruncatedFile
+    ell = 2**127 - 1
+    p = tmp_path / "big.sldv"
+    p.write_bytes(_sldv_bytes(ell, [1, 2, 3], 16, count=(1 << 64) - 1))
+    with pytest.raises(TruncatedFile):
+        load_vector(p)
+    p.write_bytes(_sldv_bytes(ell, [1, 2, 3], 16, count=(1 << 60) + 1))  # count*16 wraps to 16
+    with pytest.raises(TruncatedFile):
+        load_vector(p)

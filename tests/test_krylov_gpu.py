@@ -115,6 +115,31 @@ def test_dense_x_widths_vs_oracle(bits, extreme, tc, monkeypatch):
     assert terms[0] == [sum(a * b for a, b in zip(xv, y)) % ell for xv in xs]
 
 
+@pytest.mark.parametrize("bits", [64, 256])
+def test_dense_x_tc_at_accumulator_cap(bits, monkeypatch):
+    # every CTA of the tcgen05 digit GEMM sums the largest K the
+    # s32 TMEM accumulator allows (TC_MAX_K_PER_CTA = 32768 bytes) with
+    # 0xFF-dense digits (x = v = l - 1, l just below 2^bits): 32768 * 255^2 <
+    # 2^31, so the sums are exact without relying on wrap-around
+    monkeypatch.setenv("SLD_DENSE_TC", "1")
+    monkeypatch.setenv("SLD_TC_MAX_K", "1")
+    from paper_1402_3661_b200.modring import prev_prime
+    ell = prev_prime(1 << bits)
+    mod = PrimeModulus(ell)
+    rng = np.random.default_rng(bits)
+    n = 2 * 32768 + 4096  # 3 CTAs: two at the cap, one partial
+    A = rand_matrix(mod, rng, n, n, 4)
+    y = [ell - 1] * n
+    xs = [[ell - 1] * n for _ in range(4)]
+    X = DenseRows(xs, mod)
+    orc = to_oracle(A)
+    x = np.stack([O.ints_to_limbs(v, mod.limbs) for v in xs])
+    ot, _ = O.krylov_dense(orc, O.ints_to_limbs(y, mod.limbs), x, 3)
+    terms, _, _ = krylov_column(B200Multiplier(A), X, ints_to_planes(y, digit_count(mod.ell)), 3)
+    assert terms == [O.limbs_to_ints(t) for t in ot]
+    assert terms[0] == [n % ell] * 4
+
+
 def test_krylov_scalar_identity_and_zero():
     mod = PrimeModulus(1009)
     rng = np.random.default_rng(1)
