@@ -16,8 +16,7 @@
 #include <thread>
 #include <vector>
 
-#include "sldb200.h"
-#include "sld_ops.cuh"
+#include "sld_internal.cuh"
 
 using namespace sld;
 
@@ -25,7 +24,7 @@ using namespace sld;
 
 static thread_local std::string g_err;
 
-static int fail(int code, const char* fmt, ...) {
+int fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -34,20 +33,6 @@ static int fail(int code, const char* fmt, ...) {
   g_err = buf;
   return code;
 }
-
-#define CU(call)                                                                 \
-  do {                                                                           \
-    cudaError_t e_ = (call);                                                     \
-    if (e_ != cudaSuccess)                                                       \
-      return fail(SLD_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
-                  __FILE__, __LINE__);                                           \
-  } while (0)
-
-#define TRY(expr)              \
-  do {                         \
-    int r_ = (expr);           \
-    if (r_ != SLD_OK) return r_; \
-  } while (0)
 
 extern "C" const char* sld_last_error(void) { return g_err.c_str(); }
 // error reporting for the host-only translation units (sld_fileio.cpp)
@@ -115,138 +100,9 @@ static void hmod_u64(uint64_t c, const uint32_t* ell, int L, uint32_t* out) {
   for (int i = 0; i < L; i++) out[i] = r[i];
 }
 
-// ------------------------------------------------------------ objects
-
-struct sld_ctx {
-  int dev = 0;
-  int L = 0;
-  int SW = 0;
-  cudaStream_t stream = nullptr;   // the stream all work is issued on
-  cudaStream_t own = nullptr;      // the context's own stream
-  ModParams mp;
-  size_t l2_bytes = 0;
-  int sms = 0;
-  void* hstage = nullptr;  // pinned host staging (limb format)
-  size_t hstage_bytes = 0;
-  void* dstage = nullptr;  // device staging (limb format)
-  size_t dstage_bytes = 0;
-  size_t apw_max = 0;      // max access-policy window bytes (0: unsupported)
-  uint32_t* fold = nullptr;    // L <= 8: 2^(32k) mod ell, k = L .. TC_FOLD_TOP (lazy folds)
-  uint32_t* coef = nullptr;    // lincomb coefficient staging (64 x SW words)
-  uint8_t* die_map = nullptr;  // device copy of the %smid -> die map (256 entries)
-  int die_n[2] = {0, 0};       // SMs per die; both 0 if the map is unavailable
-  // lifetime: the owner's handle plus one reference per vector / matrix /
-  // projection block / combination set made on this context, so handles may
-  // be destroyed in any order (a garbage collector frees them in arbitrary
-  // order) without touching a freed context
-  std::atomic<int> refs{1};
-};
-
-static void ctx_free(sld_ctx* c);
-static void ctx_unref(sld_ctx* c) {
-  if (c && c->refs.fetch_sub(1) == 1) ctx_free(c);
-}
-// a context reference held by an object made on it (released on delete)
-struct CtxRef {
-  sld_ctx* c = nullptr;
-  void bind(sld_ctx* x) {
-    c = x;
-    if (c) c->refs.fetch_add(1);
-  }
-  ~CtxRef() { ctx_unref(c); }
-};
-
-struct sld_vec {
-  CtxRef ref;
-  sld_ctx* ctx = nullptr;
-  int64_t n = 0;      // residues per chain
-  int chains = 1;     // G chains interleaved per record (row*G + chain)
-  uint32_t* buf[2] = {nullptr, nullptr};
-  int cur = 0;
-};
-
-struct sld_xblock {
-  CtxRef ref;
-  sld_ctx* ctx = nullptr;
-  int m = 0;
-  int64_t n = 0;
-  uint32_t* x = nullptr;     // [t][j] SW stride: plain (L <= 8, lazy dot products) or Montgomery form
-  uint32_t* fold = nullptr;  // L <= 8: 2^(32k) mod ell for k = L .. TC_FOLD_TOP (L words each)
-  // tensor-core projection (L <= 8, m <= 16): X as pre-tiled byte digits
-  int MT = 0;                // 128-row M tiles (0: tensor-core path off)
-  int64_t ktiles = 0;        // 128-byte K tiles (K = n)
-  uint8_t* A = nullptr;      // [ktiles][MT][...] canonical K-major tiles
-  uint8_t* B = nullptr;      // per-step v digits, [ktiles][...]
-  uint32_t* partial = nullptr;
-  int nct = 0;               // CTAs (split K)
-  int64_t kt_per_cta = 0;
-};
-
-struct sld_mat {
-  CtxRef ref;
-  sld_ctx* ctx = nullptr;
-  int64_t nrows = 0, ncols = 0, total_cols = 0, nnz = 0;
-  int n_dense = 0;
-  int npass = 1;
-  int64_t stripe_cols = 0;
-  int64_t nslices = 0;
-  int64_t nslots = 0;
-  int chains = 1;  // G chains per record (built for one G)
-  int64_t n_pm = 0, n_small = 0, n_full = 0, pad_entries = 0;
-  int64_t max_deg = 0;
-  size_t dev_bytes = 0;
-  int policy = 7;  // L2 policy bits (SpmvArgs::policy), measured best; env SLD_POLICY overrides
-  int pf = 2;      // index prefetch distance in groups, measured; env SLD_PF overrides
-  int apw = 0;       // persisting L2 access-policy window over the gathered stripe (env SLD_APW)
-  float apw_ratio = 1.0f;
-  // device
-  SliceInfo* slices = nullptr;  // [npass][nslices]
-  uint4* pm_idx = nullptr;
-  uint4* s_idx = nullptr;
-  int4* s_coef = nullptr;
-  int32_t* slot_row = nullptr;
-  uint32_t* lane_k4 = nullptr;  // [pass][slot]
-  uint32_t* full_ptr = nullptr;
-  uint32_t* full_col = nullptr;
-  uint32_t* full_val = nullptr;
-  uint32_t* dense_val = nullptr;
-  uint32_t* part = nullptr;  // slot-indexed partials (npass > 1)
-  // limb-sliced passes (one chain, L > 8): T lanes per row, 32 / T rows per slice
-  int sliced = 0;
-  // short-row passes (one chain, L <= 8, small N): 4 lanes per row, 8 rows per slice
-  int short_rows = 0;
-  // die split (halves == 2): each pass's columns are dealt to the two dies
-  int halves = 1;
-  // peer push (sld_mat_set_peers): next-iterate buffers of the r grid nodes
-  int npeer = 0;
-  uint32_t* yp[8] = {nullptr};
-  int64_t peer_off = 0;
-  int64_t half_chunk = 0;      // columns per interleaved chunk
-  unsigned split_grid = 0;     // persistent CTAs of the split kernel
-  uint32_t* xch = nullptr;     // [nslots * G * SW]
-  uint32_t* cnt = nullptr;     // [nslices] arrival counters
-  uint32_t* queue = nullptr;   // [4] work queues + exit counter
-  // host-planes convenience staging
-  uint64_t* stage = nullptr;
-  size_t stage_bytes = 0;
-  sld_vec* tmp_in = nullptr;
-  sld_vec* tmp_out = nullptr;
-  // projection scratch
-  int64_t* proj_rows = nullptr;
-  int proj_cap = 0;
-  uint32_t* terms_dev = nullptr;
-  size_t terms_cap = 0;
-  // dense-X scratch
-  uint64_t* dproj_part = nullptr;
-  size_t dproj_cap = 0;
-  // fused Mksol step (sld_mat_mksol_bind): y vectors in slot order
-  uint32_t* mk_y = nullptr;
-  int mk_n = 0;
-};
-
 // -------------------------------------------------- per-L dispatch table
 
-static const LOps& ops(int L) {
+const LOps& ops(int L) {
   static LOps table[MAXL + 1];
   static bool init = [] {
     fill_ops_1_8(table);
@@ -545,7 +401,7 @@ extern "C" int sld_ctx_destroy(sld_ctx* c) {
   return SLD_OK;
 }
 
-static void ctx_free(sld_ctx* c) {
+void ctx_free(sld_ctx* c) {
   cudaSetDevice(c->dev);
   if (c->own) cudaStreamDestroy(c->own);
   if (c->die_map) cudaFree(c->die_map);
@@ -1414,8 +1270,8 @@ extern "C" int sld_mat_info(const sld_mat* m, int64_t* info) {
 // ------------------------------------------------------------- SpMV
 
 // launch all stripe passes of one product on the context stream
-static void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows,
-                           int proj_m, uint32_t* terms_out, const uint32_t* mk_coeffs = nullptr) {
+void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows,
+                    int proj_m, uint32_t* terms_out, const uint32_t* mk_coeffs) {
   sld_ctx* c = M->ctx;
   SpmvArgs a;
   memset(&a, 0, sizeof(a));
