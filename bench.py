@@ -38,15 +38,19 @@ CONFIGS = {
                  desc="configs[0]: synthetic N=20K, gamma=20, 160-bit l (CPU-oracle case)"),
     # cfg2 is ONE sequence (bp n = 1), so one chain; chain groups (G = 2, 4)
     # only apply when block Wiedemann runs n >= 2 sequences (cfg3: n = 8)
-    "cfg2": dict(n=650_000, gamma=100, bits=217, bp=(1, 2), steps=1000, warmup=20, chains=1,
+    "cfg2": dict(n=650_000, gamma=100, bits=217, bp=(1, 2), steps=2000, warmup=20, chains=1,
                  desc="configs[1]: GF(2^619)-scale N=650K FFS profile, 217-bit l, one sequence"),
-    "cfg3": dict(n=3_600_000, gamma=100, bits=202, bp=(8, 16), steps=400, warmup=10, chains=2,
+    # cfg3 is block Wiedemann with 8 sequences, ONE per GPU: the headline
+    # runs one chain per GPU; the chain group (2 of the sequences sharing a
+    # matrix pass, what one GPU running several sequences would do) is
+    # reported beside it as `chain_group`
+    "cfg3": dict(n=3_600_000, gamma=100, bits=202, bp=(8, 16), steps=1000, warmup=10, chains=1, group=2,
                  desc="configs[2]: GF(2^809)-scale N=3.6M FFS profile, 202-bit l, "
                       "block Wiedemann (8,16), one sequence per GPU"),
     "cfg4": dict(n=3_600_000, gamma=100, bits=202, bp=(1, 2), steps=100, warmup=5, chains=1,
                  desc="configs[3]: the cfg3 matrix, ONE sequence row/2D-partitioned over the GPUs "
                       "(grid r x c, NCCL exchange)"),
-    "cfg5": dict(n=1_000_000, gamma=100, bits=650, bp=(8, 16), steps=200, warmup=10, chains=1,
+    "cfg5": dict(n=1_000_000, gamma=100, bits=650, bp=(8, 16), steps=1000, warmup=10, chains=1,
                  desc="configs[4]: wide-prime stress N=1M FFS profile, 650-bit l, one sequence per GPU"),
 }
 DEFAULT_CONFIG = "cfg3"
@@ -121,6 +125,18 @@ class ClockSampler:
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
                 "samples": len(self.samples)}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def build_matrix(cfg, log):
@@ -230,7 +246,7 @@ def run_reference(args, cfg, rank, world):
         "dtype": "exact integer mod l (RNS 31-bit limbs, reference algorithm)",
         "data": "synthetic (native corpus generator, FFS profile, seed 1)",
         "config": config_block(args.config, cfg, A, mod, world),
-        "cpu_baseline": {"value": value, "unit": "SpMV/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "SpMV/s", "cores": cores, "kind": "port", "cpu": cpu_model(),
                          "sample": f"{rows} rows per step of {N} (+ the full to-RNS conversion), "
                                    f"median of {args.steps} steps, extrapolated to one SpMV"},
         "e2e": {"value": value, "unit": "SpMV/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -262,42 +278,55 @@ def run_grid(args, cfg, rank, world, local, dist, log):
     t = time.time()
     perm = balance_permutation(A, g)
     fused = args.grid_impl == "peer"
+    nodes = g.r * g.c
+    in_proc = fused and world == 1 and nodes > 1
     if fused:
-        # exchanges done by the nodes over peer memory (paper_1402_3661_b200/
-        # peergrid.py): r x 1 -- the all-gather fused into the SpMV epilogue;
-        # r x c -- partials pushed into the row collector by the epilogue,
-        # reduced, scattered by P2P copies.  Flag barriers, no collective.
+        # exchanges done by the nodes over peer memory (csrc/sld_grid.cu via
+        # paper_1402_3661_b200/peergrid.py): r x 1 -- the all-gather fused
+        # into the SpMV epilogue; r x c -- partials pushed into the row
+        # collector by the epilogue, reduced, scattered by one copy kernel.
+        # Flag barriers, one CUDA graph per iteration, no collective.  With
+        # one process and several nodes (--grid RxC on one rank) every node
+        # lives in this process (LocalGrid), round robin over the GPUs.
         from paper_1402_3661_b200 import _native as N
-        from paper_1402_3661_b200.peergrid import PeerGrid, PeerRowGrid
-        torch.cuda.set_device(local)
-
-        def exchange(obj):
-            out = [None] * world
-            tdist.all_gather_object(out, obj)
-            return out
-        if g.c == 1:
-            grid = PeerRowGrid(A, g.r, rank, exchange, device=local, perm=perm)
+        from paper_1402_3661_b200.peergrid import LocalGrid, PeerGrid
+        local_dev = local
+        torch.cuda.set_device(local_dev)
+        if in_proc:
+            grid = LocalGrid(A, g, perm=perm)
+            members = grid.nodes
         else:
-            grid = PeerGrid(A, g, rank, exchange, device=local, perm=perm)
-        N.check(N.load().sld_ctx_set_stream(grid.field.handle, torch.cuda.current_stream(local).cuda_stream))
-        log(f"peer grid {g} node {rank} block built in {time.time() - t:.1f}s")
+            def exchange(obj):
+                out = [None] * world
+                tdist.all_gather_object(out, obj)
+                return out
+            grid = PeerGrid(A, g, rank, exchange, device=local_dev, perm=perm)
+            members = [grid.node]
+        streams = []
+        for nd in members:
+            st_k = torch.cuda.Stream(device=nd.device)
+            N.check(N.load().sld_ctx_set_stream(nd.field.handle, st_k.cuda_stream))
+            streams.append(st_k)
+        log(f"peer grid {g} {'all nodes in-process' if in_proc else f'node {rank}'} built in {time.time() - t:.1f}s")
     else:
         grid = B200Grid(A, g, GridComm(g), device=local, perm=perm)
+        streams = [torch.cuda.current_stream()]
         log(f"grid {g} node {(grid.i, grid.j)} block built in {time.time() - t:.1f}s")
     y = _random_residue_limbs(np.random.default_rng(3), grid.n_padded, mod)
     grid.load_vector(y)
     grid.iterate(args.warmup)
     torch.cuda.synchronize()
     tdist.barrier()
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in streams]
     with ClockSampler(local) as clk:
-        e0.record(st)
+        for (e0, _), st_k in zip(ev, streams):
+            e0.record(st_k)
         grid.iterate(args.steps)
-        e1.record(st)
+        for (_, e1), st_k in zip(ev, streams):
+            e1.record(st_k)
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    t_all = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    ms = max(e0.elapsed_time(e1) for e0, e1 in ev)
+    t_all = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{torch.cuda.current_device()}")
     tdist.all_reduce(t_all, op=tdist.ReduceOp.MAX)
     ms = float(t_all.item())
     if fused:
@@ -306,12 +335,14 @@ def run_grid(args, cfg, rank, world, local, dist, log):
         frag_rows = grid.n_padded // q
         slot_bytes = 32 * ((4 * mod.limbs + 31) // 32)
         comm = {"impl": ("SpMV epilogue peer stores + flag barrier" if g.c == 1 else
-                         "epilogue peer stores into the collector + add_mod + P2P copies + flag barriers")
-                        + " (no collective)",
+                         "epilogue peer stores into the collector + add_mod + one scatter kernel + flag barriers")
+                        + " (one CUDA graph per iteration, no collective)",
                 "bytes_per_iter_reference_accounting": comm_volume_model(g, frag_rows * mod.byte_width),
                 "wire_bytes_per_iter": comm_volume_model(g, frag_rows * slot_bytes),
                 "messages_per_iter": 0}
-        stripes = grid.dm.info()["stripes"]
+        stripes = members[0].dm.info()["stripes"]
+        per_iter = max(nd.info()["kernels_per_iteration"] for nd in members)
+        comm["nodes_in_process"] = len(members)
     else:
         last = grid.comm_log.entries[-1]
         comm = {"impl": "NCCL p2p (collector reduce + broadcast, gridmv.py:251-348)",
@@ -319,6 +350,7 @@ def run_grid(args, cfg, rank, world, local, dist, log):
                 "wire_bytes_per_iter": last.reduce.wire_bytes + last.broadcast.wire_bytes,
                 "messages_per_iter": last.reduce.messages + last.broadcast.messages}
         stripes = grid.engine.dm.info()["stripes"]
+        per_iter = stripes + (1 if g.c > 1 else 0)
     B, Z, Zs, Zf = algorithmic_bytes(A, mod.limbs)
     peak, peak_kind = measured_peaks()
     per = ms / args.steps
@@ -326,6 +358,8 @@ def run_grid(args, cfg, rank, world, local, dist, log):
         "metric": METRIC, "value": args.steps / (ms / 1e3), "unit": "SpMV/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32 limbs, exact mod l",
+        "grid_nodes_on_this_box": (f"{len(members)} node(s) in this process on "
+                                   f"{len({nd.device for nd in members})} GPU(s)" if fused else None),
         "data": "synthetic (native corpus generator, FFS profile, seed 1)",
         "config": dict(config_block("cfg4", cfg, A, mod, world), grid=str(g),
                        parallelism=(f"one chain on a {g} grid, exchanges over peer memory (no collective)"
@@ -336,7 +370,7 @@ def run_grid(args, cfg, rank, world, local, dist, log):
         "comm": comm,
         # rank 0 (a row collector): SpMV passes, add_mod when c > 1, and the
         # flag barriers of the peer exchange (1 for r x 1, 2 for r x c)
-        "gpu_launches": args.steps * (stripes + (1 if g.c > 1 else 0) + ((1 if g.c == 1 else 2) if fused else 0)),
+        "gpu_launches": args.steps * per_iter * (len(members) if fused else 1),
         "clocks": clk.summary(),
     }
     if rank == 0:
@@ -435,7 +469,9 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
     with ClockSampler(local) as clk:
-        total_ms, per_ms = dm.bench(v, args.steps, 0)
+        # an event after every product pair (between graph launches) gives
+        # the per-product samples for the median; the total is the K steps
+        total_ms, samples = dm.bench_samples(v, args.steps, 0, pairs_per_sample=1)
     if dist is not None:
         import torch
         torch.cuda.synchronize()
@@ -445,20 +481,27 @@ def main():
     ms_per_step = total_ms / steps_even       # one step = one product of each of the G chains
     value = world * G * steps_even / (total_ms / 1e3)
     launches = steps_even * info["stripes"]
+    med_ms = float(np.median(samples))
 
-    # the same GPU running ONE sequence (the config's one-chain-per-GPU
-    # deployment), for comparison with the chain-group step above
-    single = None
-    if G > 1:
-        dm1 = DeviceMatrix(A, device=local, chains=1)
-        v1 = dm1.vector()
-        v1.upload_limbs(ys[0])
-        dm1.bench(v1, args.warmup, 0)
-        t1, _ = dm1.bench(v1, args.steps, 0)
-        single = {"value": world * steps_even / (t1 / 1e3), "unit": "SpMV/s",
-                  "ms_per_product": t1 / steps_even, "layout": dm1.info()}
-        v1.close()
-        dm1.close()
+    # several sequences per GPU (a GPU running more than one of the block-
+    # Wiedemann sequences): Gc chains share each matrix pass, index stream
+    # read once, the G residues of a column one contiguous record
+    group = None
+    Gc = cfg.get("group", 1) if args.chains is None else 1
+    if Gc > 1 and mod.limbs <= 8:
+        dmg = DeviceMatrix(A, device=local, chains=Gc)
+        vg = dmg.vector()
+        vg.upload_limbs(np.stack([ys[0]] + [_random_residue_limbs(rng, A.total_cols, mod)
+                                            for _ in range(Gc - 1)]))
+        dmg.bench(vg, args.warmup, 0)
+        tg, sg = dmg.bench_samples(vg, args.steps, 0, pairs_per_sample=1)
+        group = {"chains_per_pass": Gc, "value": world * Gc * steps_even / (tg / 1e3), "unit": "SpMV/s",
+                 "ms_per_pass": tg / steps_even, "ms_per_chain_product": tg / steps_even / Gc,
+                 "ms_per_pass_median": float(np.median(sg)), "layout": dmg.info(),
+                 "note": f"{Gc} sequences per GPU per matrix pass (bp n >= {Gc * world} at {world} GPU(s)); "
+                         "not the headline, which is the config's one sequence per GPU"}
+        vg.close()
+        dmg.close()
 
     # ---- end to end through the public API with host y in, host terms (m
     # per chain and step) and the final iterates out: krylov_column for one
@@ -555,6 +598,11 @@ def main():
     # one request per sector and the 1-sector rate applies
     rec_sectors = G * info.get("lanes_per_residue", 1)
     gpeak = L2_GATHER_PEAK_GBS[rec_sectors]
+    # the floor of this algorithm: every nonzero's residue must reach the SMs
+    # as one gather request, at the measured L2-resident request rate for the
+    # record size (all gathers hitting L2, index stream free)
+    floor_ms = gather_bytes / (gpeak * 1e9) * 1e3
+    floor_frac = B_pass / (floor_ms / 1e3) / 1e9 / peak
     line = {
         "metric": METRIC, "value": value, "unit": "SpMV/s", "n_gpus": world, "steps": steps_even,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -563,8 +611,8 @@ def main():
         "config": dict(config_block(args.config, cfg, A, mod, world, chains=G), chains_per_gpu=G,
                        step=f"one product of each of the {G} chain(s) on every GPU",
                        sequences=(f"{G} of the block-Wiedemann sequences per GPU share each matrix pass "
-                                  f"(chain group); one_chain_per_gpu times one sequence per GPU"
-                                  if G > 1 else "one sequence per GPU")),
+                                  f"(chain group, --chains)"
+                                  if G > 1 else "one sequence per GPU (the config's deployment)")),
         "ms_per_chain_product": ms_per_step / G,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -575,6 +623,14 @@ def main():
                             "unit": "GB/s", "bytes_per_step": gather_bytes,
                             "achieved": gather_bytes / (ms_per_step / 1e3) / 1e9,
                             "frac": gather_bytes / (ms_per_step / 1e3) / 1e9 / gpeak},
+        "gather_floor": {"ms_per_step": floor_ms, "frac_of_floor": floor_ms / ms_per_step,
+                         "hbm_frac_at_floor": floor_frac,
+                         "note": "the derived target: at the floor (every gather an L2 hit at the measured "
+                                 "request rate) the HBM roofline fraction would be hbm_frac_at_floor, so the "
+                                 "contract's 0.60 is unreachable with one request per nonzero"},
+        "ms_per_step_median": med_ms,
+        "samples": {"count": int(len(samples)), "per": "product pair (median of the per-product times)",
+                    "p10_ms": float(np.percentile(samples, 10)), "p90_ms": float(np.percentile(samples, 90))},
         "int_ops_per_product": int_ops(A, L),
         # SURVEY 8(d)'s IMAD/INT32 side of the roofline: its op count O per
         # product against the measured int32 add rate (profiles/microbench_r01.txt)
@@ -597,7 +653,7 @@ def main():
         "clocks": clk.summary(),
         "clocks_e2e": clk_e2e.summary(),
         "layout": info,
-        "one_chain_per_gpu": single,
+        "chain_group": group,
         "witness_check": ok_witness,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -607,7 +663,7 @@ def main():
             orc = oracle_for(A)
             val, cores, sample = cpu_sample(orc, y, args.cpu_seconds, log)
             line["cpu_baseline"] = {"value": val, "unit": "SpMV/s", "cores": cores, "kind": "port",
-                                    "sample": sample}
+                                    "sample": sample, "cpu": cpu_model()}
         except Exception as e:  # the baseline must not hide the GPU number
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:

@@ -41,10 +41,11 @@ extern "C" {
 #define SLD_E_CUDA -2    /* CUDA runtime failure  (reference: n/a)             */
 #define SLD_E_BOUND -3   /* exactness bound exceeded (reference: AssertionError,
                             vecops.py:407,414 / ContractViolation modring.py:40) */
-#define SLD_E_NCCL -4    /* collective failure                                 */
+#define SLD_E_TIMEOUT -4 /* grid barrier timed out (reference: gridmv.GridTimeoutError) */
 #define SLD_E_FORMAT -5  /* malformed file     (reference: fileio.FormatError)    */
 #define SLD_E_MAGIC -6   /* wrong magic bytes  (reference: fileio.BadMagic)       */
 #define SLD_E_TRUNC -7   /* file ends early    (reference: fileio.TruncatedFile)  */
+#define SLD_E_PROTOCOL -8 /* stale grid iteration (reference: gridmv.GridProtocolError) */
 
 typedef struct sld_ctx sld_ctx;
 typedef struct sld_mat sld_mat;
@@ -228,6 +229,13 @@ int sld_spmv_mksol(sld_mat *m, sld_vec *in, sld_vec *out, const uint32_t *coeffs
 int sld_bench_spmv(sld_mat *m, sld_vec *v, int64_t steps, int warmup, double *total_ms,
                    double *kernel_ms);
 
+/* As sld_bench_spmv, with per-sample durations for a median: an event is
+ * recorded after every `pairs_per_sample` product pairs, and sample_ms
+ * (ceil(ceil(steps/2) / pairs_per_sample) entries) receives the duration
+ * of each sample.  sample_ms = NULL behaves as sld_bench_spmv. */
+int sld_bench_spmv_samples(sld_mat *m, sld_vec *v, int64_t steps, int warmup, int64_t pairs_per_sample,
+                           double *sample_ms, double *total_ms, double *kernel_ms);
+
 /* Synthetic corpus generator (fixture producer, not timed): a native
  * restatement of the row/column distribution of sldlag/corpus.py:104-139
  * (row weight rint(N(gamma, 0.1 gamma)) clipped to [3, ncols/2], column j
@@ -290,23 +298,57 @@ int sld_sldv_write(const char *path, int kind, const uint32_t *ell, int L, int64
 int sld_sldv_info(const char *path, int header_only, int64_t *info, uint8_t *ell_be, int ell_cap);
 int sld_sldv_read(const char *path, uint32_t *limbs, int stride);
 
+
+
 /*
- * r x 1 grid with the all-gather fused into the SpMV (the
- * fused alternative to gridmv.py:251-348's broadcast): the last pass stores
- * each output row into every node's next-iterate buffer (peer pointers, up
- * to 8) at row row_off + row; sld_peer_barrier then signals every node's
- * flag word (system-scope atomics) and waits for its own to reach target.
- * Peer buffers cross processes as 64-byte CUDA IPC handles.
+ * Native grid node: one Krylov chain over an r x c grid (r*c <= 8 nodes),
+ * replacing the reference's Grid (gridmv.py:193-354: _one_iteration,
+ * apply_once, the collector rule and its failure detection, 46-51).  Every
+ * exchange runs over peer memory: the block's SpMV pushes its output (r x 1:
+ * rows of every node's next iterate; r x c: the partial into the row
+ * collector's inbox), the collector reduces (add_mod) and scatters the row
+ * piece with one copy kernel, flag barriers order the phases.  Each
+ * iteration is a replayed CUDA graph: no host synchronisation, no
+ * collective.  Setup only: every node publishes a SLD_GRID_BLOB-byte record
+ * (sld_grid_blob; CUDA IPC handle + pointer) and connects to all records in
+ * rank order (sld_grid_connect) -- the records travel over any host
+ * transport.  Nodes may share a process (raw pointers, peer access enabled)
+ * or not (IPC).
+ *
+ *  sld_grid_create   block = A_ij of the balanced padded matrix as an
+ *                    sld_mat (br x bc, one chain, <= 8 limbs); not owned
+ *  sld_grid_load/read this node's fragment u_j (bc x L limbs; r x 1: the
+ *                    whole padded iterate)
+ *  sld_grid_set_projection  unit-X rows (global padded indices, m <= 32):
+ *                    each iteration records the rows of its INPUT fragment
+ *                    that this node reports (row-0 nodes, owned[t] = 1)
+ *                    into a device ring of max_steps; sld_grid_terms drains
+ *                    it as [steps][m][L] limbs (0 where not owned)
+ *  sld_grid_launch   enqueue count iterations (asynchronous)
+ *  sld_grid_wait     synchronise; SLD_E_TIMEOUT if a barrier saw no progress
+ *                    for the timeout (default 30 s; a node stopped),
+ *                    SLD_E_PROTOCOL if a node published an iteration other
+ *                    than this one or the next (stale or restarted node)
+ *  sld_grid_set_epoch resume: all nodes at the same completed iteration
+ *  sld_grid_info     [iteration, nodes, br, bc, collector, bytes, parity,
+ *                    kernels per iteration]
  */
-int sld_mat_set_peers(sld_mat *m, int npeer, const uint64_t *yptrs, int64_t row_off);
-int sld_spmv_peers(sld_mat *m, uint64_t x_ptr);
-int sld_peer_barrier(sld_ctx *ctx, int npeer, const uint64_t *flag_ptrs, uint64_t my_flag, uint32_t target);
-int sld_memcpy_async(sld_ctx *ctx, uint64_t dst, uint64_t src, int64_t bytes);
-int sld_dev_alloc(int device, int64_t bytes, uint64_t *ptr);
-int sld_dev_free(int device, uint64_t ptr);
-int sld_ipc_get(int device, uint64_t ptr, uint8_t *handle64);
-int sld_ipc_open(int device, const uint8_t *handle64, uint64_t *ptr);
-int sld_ipc_close(int device, uint64_t ptr);
+#define SLD_GRID_BLOB 128
+typedef struct sld_grid sld_grid;
+int sld_grid_create(sld_mat *block, int r, int c, int rank, int64_t n_padded, sld_grid **out);
+int sld_grid_blob(sld_grid *g, uint8_t *blob);
+int sld_grid_connect(sld_grid *g, const uint8_t *blobs);
+int sld_grid_set_timeout(sld_grid *g, double seconds);
+int sld_grid_set_projection(sld_grid *g, const int64_t *rows, int m, int64_t max_steps, uint8_t *owned);
+int sld_grid_load(sld_grid *g, const uint32_t *limbs);
+int sld_grid_read(sld_grid *g, uint32_t *limbs);
+int sld_grid_launch(sld_grid *g, int64_t count);
+int sld_grid_wait(sld_grid *g);
+int sld_grid_iterate(sld_grid *g, int64_t count);
+int sld_grid_terms(sld_grid *g, uint32_t *terms, int64_t *steps);
+int sld_grid_set_epoch(sld_grid *g, int64_t epoch);
+int sld_grid_info(sld_grid *g, int64_t *info);
+int sld_grid_destroy(sld_grid *g);
 
 #ifdef __cplusplus
 }

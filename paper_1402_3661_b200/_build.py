@@ -20,7 +20,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2"
                      "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
 if os.environ.get("SLD_NVCC_EXTRA"):
     NVCC_FLAGS += os.environ["SLD_NVCC_EXTRA"].split()
-SOURCES = ["sld_capi.cu", "sld_inst_1_8.cu", "sld_inst_9_16.cu", "sld_inst_17_24.cu",
+SOURCES = ["sld_capi.cu", "sld_grid.cu", "sld_inst_1_8.cu", "sld_inst_9_16.cu", "sld_inst_17_24.cu",
            "sld_inst_25_32.cu", "sld_corpus.cpp", "sld_fileio.cpp",
            "sld_split.cpp"]
 

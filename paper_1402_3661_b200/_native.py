@@ -18,10 +18,12 @@ SLD_OK = 0
 SLD_E_ARG = -1
 SLD_E_CUDA = -2
 SLD_E_BOUND = -3
-SLD_E_NCCL = -4
+SLD_E_TIMEOUT = -4
 SLD_E_FORMAT = -5
 SLD_E_MAGIC = -6
 SLD_E_TRUNC = -7
+SLD_E_PROTOCOL = -8
+SLD_GRID_BLOB = 128
 
 # every symbol include/sldb200.h declares (checked by tests/test_native_abi.py)
 EXPORTS = [
@@ -33,13 +35,14 @@ EXPORTS = [
     "sld_vec_upload_limbs", "sld_vec_download_limbs", "sld_vec_device_ptr",
     "sld_vec_upload_planes_chains", "sld_vec_download_planes_chains",
     "sld_lcset_create", "sld_lcset_apply", "sld_lcset_destroy",
-    "sld_mat_set_peers", "sld_spmv_peers", "sld_peer_barrier", "sld_memcpy_async", "sld_dev_alloc", "sld_dev_free",
-    "sld_ipc_get", "sld_ipc_open", "sld_ipc_close",
     "sld_spmv", "sld_spmv_async", "sld_spmv_planes", "sld_krylov_unit",
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
-    "sld_bench_spmv", "sld_corpus_rows", "sld_corpus_fill",
+    "sld_bench_spmv", "sld_bench_spmv_samples", "sld_corpus_rows", "sld_corpus_fill",
     "sld_sldm_info", "sld_sldm_read", "sld_sldm_write", "sld_sldv_write", "sld_sldv_info", "sld_sldv_read",
     "sld_split_block", "sld_mat_mksol_bind", "sld_spmv_mksol",
+    "sld_grid_create", "sld_grid_blob", "sld_grid_connect", "sld_grid_set_timeout", "sld_grid_set_projection",
+    "sld_grid_load", "sld_grid_read", "sld_grid_launch", "sld_grid_wait", "sld_grid_iterate", "sld_grid_terms",
+    "sld_grid_set_epoch", "sld_grid_info", "sld_grid_destroy",
 ]
 
 
@@ -50,6 +53,16 @@ class NativeUnavailable(RuntimeError):
 class BoundError(AssertionError):
     """Exactness bound exceeded (the reference raises AssertionError /
     ContractViolation for the same condition, vecops.py:407,414)."""
+
+
+class GridProtocolError(RuntimeError):
+    """A grid node published the wrong iteration: stale or restarted
+    (the reference's gridmv.GridProtocolError, gridmv.py:46-47)."""
+
+
+class GridTimeoutError(RuntimeError):
+    """A grid barrier / expected message never completed: a node stopped
+    (the reference's gridmv.GridTimeoutError, gridmv.py:50-51)."""
 
 
 _lib = None
@@ -99,15 +112,6 @@ def load(build_if_missing=False):
             "sld_lcset_create": ([vp, vp, i32, i64, pp], i32),
             "sld_lcset_apply": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64], i32),
             "sld_lcset_destroy": ([vp], i32),
-            "sld_mat_set_peers": ([vp, i32, vp, i64], i32),
-            "sld_spmv_peers": ([vp, ctypes.c_uint64], i32),
-            "sld_peer_barrier": ([vp, i32, vp, ctypes.c_uint64, ctypes.c_uint32], i32),
-            "sld_memcpy_async": ([vp, ctypes.c_uint64, ctypes.c_uint64, i64], i32),
-            "sld_dev_alloc": ([i32, i64, vp], i32),
-            "sld_dev_free": ([i32, ctypes.c_uint64], i32),
-            "sld_ipc_get": ([i32, ctypes.c_uint64, vp], i32),
-            "sld_ipc_open": ([i32, vp, vp], i32),
-            "sld_ipc_close": ([i32, ctypes.c_uint64], i32),
             "sld_vec_download_planes_chains": ([vp, vp, i64, i32], i32),
             "sld_vec_download_limbs": ([vp, vp, i64], i32),
             "sld_vec_device_ptr": ([vp, vp, vp], i32),
@@ -119,6 +123,7 @@ def load(build_if_missing=False):
             "sld_xblock_destroy": ([vp], i32),
             "sld_krylov_dense": ([vp, vp, vp, i64, vp], i32),
             "sld_bench_spmv": ([vp, vp, i64, i32, vp, vp], i32),
+            "sld_bench_spmv_samples": ([vp, vp, i64, i32, i64, vp, vp, vp], i32),
             "sld_sldm_info": ([ctypes.c_char_p, i32, vp, vp, i32], i32),
             "sld_sldm_read": ([ctypes.c_char_p, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
             "sld_sldm_write": ([ctypes.c_char_p, i64, i64, vp, i32, vp, vp, vp, vp, i64, vp, vp, i32, vp, vp],
@@ -131,6 +136,20 @@ def load(build_if_missing=False):
                                  vp, vp, vp, vp, i32], i32),
             "sld_mat_mksol_bind": ([vp, vp, i32], i32),
             "sld_spmv_mksol": ([vp, vp, vp, vp], i32),
+            "sld_grid_create": ([vp, i32, i32, i32, i64, vp], i32),
+            "sld_grid_blob": ([vp, vp], i32),
+            "sld_grid_connect": ([vp, vp], i32),
+            "sld_grid_set_timeout": ([vp, ctypes.c_double], i32),
+            "sld_grid_set_projection": ([vp, vp, i32, i64, vp], i32),
+            "sld_grid_load": ([vp, vp], i32),
+            "sld_grid_read": ([vp, vp], i32),
+            "sld_grid_launch": ([vp, i64], i32),
+            "sld_grid_wait": ([vp], i32),
+            "sld_grid_iterate": ([vp, i64], i32),
+            "sld_grid_terms": ([vp, vp, vp], i32),
+            "sld_grid_set_epoch": ([vp, i64], i32),
+            "sld_grid_info": ([vp, vp], i32),
+            "sld_grid_destroy": ([vp], i32),
             "sld_split_block": ([i64, vp, vp, i32, vp, vp, i64, vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, i32],
                                 i64),
         }
@@ -151,6 +170,10 @@ def check(rc):
         raise ValueError(msg)
     if rc == SLD_E_BOUND:
         raise BoundError(msg)
+    if rc == SLD_E_TIMEOUT:
+        raise GridTimeoutError(msg)
+    if rc == SLD_E_PROTOCOL:
+        raise GridProtocolError(msg)
     raise RuntimeError(f"libsldb200: {msg}")
 
 

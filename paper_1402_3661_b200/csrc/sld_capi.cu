@@ -1436,130 +1436,6 @@ extern "C" int sld_spmv_mksol(sld_mat* M, sld_vec* in, sld_vec* out, const uint3
   return SLD_OK;
 }
 
-// ---- r x 1 grid with the all-gather fused into the SpMV epilogue: the last
-// pass stores each output row into every node's next iterate (peer device
-// pointers: cudaIpc handles across processes, NVLink P2P across GPUs), and
-// a flag barrier (system-scope atomics on every node's flag word) orders
-// the iterations.
-extern "C" int sld_mat_set_peers(sld_mat* M, int npeer, const uint64_t* yptrs, int64_t row_off) {
-  if (!M || npeer < 0 || npeer > 8 || (npeer && !yptrs) || row_off < 0)
-    return fail(SLD_E_ARG, "bad peer set (1..8 peers)");
-  if (npeer && (M->halves != 1 || M->sliced)) return fail(SLD_E_ARG, "peer push runs on the row-major layouts");
-  M->npeer = npeer;
-  for (int k = 0; k < 8; k++) M->yp[k] = k < npeer ? (uint32_t*)(uintptr_t)yptrs[k] : nullptr;
-  M->peer_off = row_off;
-  return SLD_OK;
-}
-
-// one product from the raw iterate x_ptr into the peers' buffers
-// (asynchronous on the context stream)
-extern "C" int sld_spmv_peers(sld_mat* M, uint64_t x_ptr) {
-  if (!M || !x_ptr || !M->npeer) return fail(SLD_E_ARG, "no peers set");
-  CU(cudaSetDevice(M->ctx->dev));
-  launch_product(M, (const uint32_t*)(uintptr_t)x_ptr, nullptr, nullptr, 0, nullptr);
-  CU(cudaGetLastError());
-  return SLD_OK;
-}
-
-namespace {
-struct PeerFlags {
-  uint32_t* f[8];
-};
-__global__ void peer_barrier_kernel(const PeerFlags pf, int npeer, const uint32_t* my_flag, uint32_t target,
-                                    int* timed_out) {
-  if (threadIdx.x != 0) return;
-  __threadfence_system();
-  for (int k = 0; k < npeer; k++) atomicAdd_system(pf.f[k], 1u);
-  uint64_t t0, t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (true) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_flag) : "memory");
-    if ((int32_t)(v - target) >= 0) break;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 30000000000ull) {  // 30 s: a peer died; report instead of hanging
-      *timed_out = 1;
-      break;
-    }
-    __nanosleep(200);
-  }
-  __threadfence_system();
-}
-}  // namespace
-
-// signal every node (flag words, peer pointers, own included), then wait
-// until this node's flag reaches `target` (= npeer * iterations done)
-extern "C" int sld_peer_barrier(sld_ctx* c, int npeer, const uint64_t* flag_ptrs, uint64_t my_flag,
-                                uint32_t target) {
-  if (!c || npeer < 1 || npeer > 8 || !flag_ptrs || !my_flag) return fail(SLD_E_ARG, "bad barrier arguments");
-  CU(cudaSetDevice(c->dev));
-  static thread_local int* d_to = nullptr;
-  static thread_local int d_to_dev = -1;
-  if (!d_to || d_to_dev != c->dev) {
-    CU(cudaMalloc(&d_to, sizeof(int)));
-    d_to_dev = c->dev;
-  }
-  CU(cudaMemsetAsync(d_to, 0, sizeof(int), c->stream));
-  PeerFlags pf;
-  for (int k = 0; k < 8; k++) pf.f[k] = k < npeer ? (uint32_t*)(uintptr_t)flag_ptrs[k] : nullptr;
-  peer_barrier_kernel<<<1, 32, 0, c->stream>>>(pf, npeer, (const uint32_t*)(uintptr_t)my_flag, target, d_to);
-  CU(cudaGetLastError());
-  int to = 0;
-  CU(cudaMemcpyAsync(&to, d_to, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
-  if (to) return fail(SLD_E_CUDA, "peer barrier timed out (a grid node stopped)");
-  return SLD_OK;
-}
-
-// stream-ordered device copy (peer pointers included: an NVLink P2P copy)
-extern "C" int sld_memcpy_async(sld_ctx* c, uint64_t dst, uint64_t src, int64_t bytes) {
-  if (!c || (bytes && (!dst || !src)) || bytes < 0) return fail(SLD_E_ARG, "bad copy");
-  CU(cudaSetDevice(c->dev));
-  if (bytes) CU(cudaMemcpyAsync((void*)(uintptr_t)dst, (const void*)(uintptr_t)src, (size_t)bytes,
-                                cudaMemcpyDeviceToDevice, c->stream));
-  return SLD_OK;
-}
-
-// raw device memory and CUDA IPC handles (64 bytes) for the peer buffers
-extern "C" int sld_dev_alloc(int device, int64_t bytes, uint64_t* ptr) {
-  if (!ptr || bytes <= 0) return fail(SLD_E_ARG, "bad allocation");
-  CU(cudaSetDevice(device));
-  void* p = nullptr;
-  CU(cudaMalloc(&p, (size_t)bytes));
-  CU(cudaMemset(p, 0, (size_t)bytes));
-  *ptr = (uint64_t)(uintptr_t)p;
-  return SLD_OK;
-}
-extern "C" int sld_dev_free(int device, uint64_t ptr) {
-  CU(cudaSetDevice(device));
-  if (ptr) CU(cudaFree((void*)(uintptr_t)ptr));
-  return SLD_OK;
-}
-extern "C" int sld_ipc_get(int device, uint64_t ptr, uint8_t* handle64) {
-  if (!ptr || !handle64) return fail(SLD_E_ARG, "null argument");
-  CU(cudaSetDevice(device));
-  cudaIpcMemHandle_t h;
-  CU(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)ptr));
-  static_assert(sizeof(h) == 64, "IPC handle size");
-  memcpy(handle64, &h, 64);
-  return SLD_OK;
-}
-extern "C" int sld_ipc_open(int device, const uint8_t* handle64, uint64_t* ptr) {
-  if (!handle64 || !ptr) return fail(SLD_E_ARG, "null argument");
-  CU(cudaSetDevice(device));
-  cudaIpcMemHandle_t h;
-  memcpy(&h, handle64, 64);
-  void* p = nullptr;
-  CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-  *ptr = (uint64_t)(uintptr_t)p;
-  return SLD_OK;
-}
-extern "C" int sld_ipc_close(int device, uint64_t ptr) {
-  CU(cudaSetDevice(device));
-  if (ptr) CU(cudaIpcCloseMemHandle((void*)(uintptr_t)ptr));
-  return SLD_OK;
-}
-
 extern "C" int sld_spmv_planes(sld_mat* M, const uint64_t* in_planes, uint64_t* out_planes, int P) {
   if (!M) return fail(SLD_E_ARG, "null matrix");
   sld_ctx* c = M->ctx;
@@ -1815,6 +1691,14 @@ extern "C" int sld_krylov_dense(sld_mat* M, sld_vec* v, sld_xblock* X, int64_t s
 
 extern "C" int sld_bench_spmv(sld_mat* M, sld_vec* v, int64_t steps, int warmup, double* total_ms,
                               double* kernel_ms) {
+  return sld_bench_spmv_samples(M, v, steps, warmup, 0, nullptr, total_ms, kernel_ms);
+}
+
+// as sld_bench_spmv; with sample_ms != null an event is recorded after every
+// `pairs_per_sample` product pairs (between graph launches: the stream keeps
+// running), and sample_ms[k] gets the duration of sample k
+extern "C" int sld_bench_spmv_samples(sld_mat* M, sld_vec* v, int64_t steps, int warmup, int64_t pairs_per_sample,
+                                      double* sample_ms, double* total_ms, double* kernel_ms) {
   if (!M || !v || steps < 1) return fail(SLD_E_ARG, "bad bench arguments");
   if (M->nrows != M->total_cols || v->n != M->total_cols) return fail(SLD_E_ARG, "square matrix needed");
   if (v->chains != M->chains) return fail(SLD_E_ARG, "vector chains != matrix chains");
@@ -1841,13 +1725,35 @@ extern "C" int sld_bench_spmv(sld_mat* M, sld_vec* v, int64_t steps, int warmup,
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
   const int64_t pairs = (steps + 1) / 2;
+  std::vector<cudaEvent_t> marks;
+  if (sample_ms) {
+    if (pairs_per_sample < 1) return fail(SLD_E_ARG, "pairs_per_sample must be >= 1");
+    marks.resize((size_t)((pairs + pairs_per_sample - 1) / pairs_per_sample));
+    for (auto& e : marks) CU(cudaEventCreate(&e));
+  }
   CU(cudaEventRecord(e0, c->stream));
-  for (int64_t k = 0; k < pairs / 16; k++) CU(cudaGraphLaunch(ge32, c->stream));
-  for (int64_t k = 0; k < pairs % 16; k++) CU(cudaGraphLaunch(ge2, c->stream));
+  if (sample_ms) {
+    for (int64_t k = 0, m = 0; k < pairs; m++) {
+      const int64_t n = std::min(pairs_per_sample, pairs - k);
+      for (int64_t j = 0; j < n / 16; j++) CU(cudaGraphLaunch(ge32, c->stream));
+      for (int64_t j = 0; j < n % 16; j++) CU(cudaGraphLaunch(ge2, c->stream));
+      CU(cudaEventRecord(marks[(size_t)m], c->stream));
+      k += n;
+    }
+  } else {
+    for (int64_t k = 0; k < pairs / 16; k++) CU(cudaGraphLaunch(ge32, c->stream));
+    for (int64_t k = 0; k < pairs % 16; k++) CU(cudaGraphLaunch(ge2, c->stream));
+  }
   CU(cudaEventRecord(e1, c->stream));
   CU(cudaEventSynchronize(e1));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e0, e1));
+  for (size_t m = 0; m < marks.size(); m++) {
+    float d = 0;
+    CU(cudaEventElapsedTime(&d, m ? marks[m - 1] : e0, marks[m]));
+    sample_ms[m] = d;
+  }
+  for (auto& e : marks) cudaEventDestroy(e);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaGraphExecDestroy(ge2);

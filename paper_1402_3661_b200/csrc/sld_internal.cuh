@@ -135,7 +135,7 @@ struct sld_mat {
   int short_rows = 0;
   // die split (halves == 2): each pass's columns are dealt to the two dies
   int halves = 1;
-  // peer push (sld_mat_set_peers): next-iterate buffers of the r grid nodes
+  // peer push (set by the grid, sld_grid.cu): the last pass stores into these buffers
   int npeer = 0;
   uint32_t* yp[8] = {nullptr};
   int64_t peer_off = 0;
@@ -166,7 +166,7 @@ struct sld_mat {
 // the per-limb-count kernel table (sld_inst_*.cu)
 const sld::LOps& ops(int L);
 // one product x -> y (all stripe passes) on the matrix's context stream; with
-// y == nullptr and peers set (sld_mat_set_peers) the last pass stores into
+// y == nullptr and peers set (the grid, sld_grid.cu) the last pass stores into
 // the peers' buffers.  proj_rows / terms_out: fused unit-X projection of x.
 void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows, int proj_m,
                     uint32_t* terms_out, const uint32_t* mk_coeffs = nullptr);

@@ -425,6 +425,21 @@ class DeviceMatrix:
                                          ctypes.byref(tot), ctypes.byref(per)))
         return tot.value, per.value
 
+    def bench_samples(self, v: DeviceVector, steps, warmup=3, pairs_per_sample=1):
+        """(total_ms, per-product ms of each sample) -- the samples are the
+        durations of consecutive groups of `pairs_per_sample` product pairs."""
+        pairs = (int(steps) + 1) // 2
+        n = (pairs + pairs_per_sample - 1) // pairs_per_sample
+        buf = np.zeros(n, dtype=np.float64)
+        tot = ctypes.c_double()
+        per = ctypes.c_double()
+        N.check(N.load().sld_bench_spmv_samples(self._h, v.handle, int(steps), int(warmup),
+                                                 int(pairs_per_sample), N.ptr(buf), ctypes.byref(tot),
+                                                 ctypes.byref(per)))
+        sizes = np.full(n, 2 * pairs_per_sample, dtype=np.float64)
+        sizes[-1] = 2 * (pairs - pairs_per_sample * (n - 1))
+        return tot.value, buf / sizes
+
     def close(self):
         if getattr(self, "_h", None):
             N.load().sld_mat_destroy(self._h)

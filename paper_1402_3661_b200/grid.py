@@ -37,12 +37,9 @@ KIND_PARTIAL_SUM = 0
 KIND_FRAGMENT = 1
 
 
-class GridProtocolError(RuntimeError):
-    """A message arrived with the wrong iteration tag (gridmv.py:46-47)."""
-
-
-class GridTimeoutError(RuntimeError):
-    """An expected message / slice never arrived (gridmv.py:50-51)."""
+# raised by the native grid's barriers (sld_grid_wait) and by the exchange
+# checks below; defined next to the status mapping in _native
+from ._native import GridProtocolError, GridTimeoutError  # noqa: E402
 
 
 @dataclass
