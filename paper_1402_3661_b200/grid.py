@@ -15,9 +15,9 @@ One process per GPU (torch.distributed, rank = i*c + j).  The exchange
 schedule, the collector rule and the message/byte log (CommLog, the
 reference's accounting: rows x byte_width, gridmv.py:151-176) follow the
 reference, so `comm_volume_model` predicts the bytes exactly.  Failure
-detection mirrors gridmv.py:46-51: a wrong iteration tag raises
-GridProtocolError, a missing slice GridTimeoutError (NCCL's own timeout
-covers a dead peer).
+detection mirrors gridmv.py:46-51: every p2p payload travels behind its tag
+(iteration, kind, source), a wrong tag raises GridProtocolError, a message
+that does not arrive within GridComm's timeout GridTimeoutError.
 
 The compute and buffer side is an *engine*: `DeviceEngine` runs on
 libsldb200 (device fragments, CUDA kernels); tests substitute a CPU engine
@@ -142,7 +142,9 @@ class GridComm:
     backend (gloo) and device tensors, payloads are staged through host
     memory."""
 
-    def __init__(self, g: GridSpec, group=None):
+    def __init__(self, g: GridSpec, group=None, timeout=300.0):
+        import datetime
+
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
@@ -153,12 +155,22 @@ class GridComm:
         if self.world != g.r * g.c:
             raise ValueError(f"grid {g} needs {g.r * g.c} ranks, have {self.world}")
         self.staged = dist.get_backend(group) != "nccl"
+        self.timeout = datetime.timedelta(seconds=float(timeout))
 
     def rank_of(self, i, j):
         return i * self.g.c + j
 
-    def exchange(self, sends, recvs):
-        """sends: [(tensor, dst)], recvs: [(tensor, src)] as one p2p batch."""
+    def header(self, iteration, kind, like):
+        """A message's tag (gridmv.py Message: kind, src, iteration)."""
+        dev = "cpu" if self.staged or not like.is_cuda else like.device
+        return self.torch.tensor([iteration, kind, self.rank], dtype=self.torch.int64, device=dev)
+
+    def exchange(self, sends, recvs, iteration=None, kind=None):
+        """sends: [(tensor, dst)], recvs: [(tensor, src)] as one p2p batch.
+        With `iteration`, every payload travels behind its tag (iteration,
+        kind, src) and a received tag other than the expected one raises
+        GridProtocolError (gridmv.py:276-283); a message that does not
+        arrive within the timeout raises GridTimeoutError (gridmv.py:285-290)."""
         dist = self.dist
         if not sends and not recvs:
             return
@@ -167,10 +179,28 @@ class GridComm:
             r2 = [(self.torch.empty(t.shape, dtype=t.dtype) if t.is_cuda else t, s) for t, s in recvs]
         else:
             s2, r2 = sends, recvs
-        ops = [dist.P2POp(dist.isend, t, d, self.group) for t, d in s2]
+        ops = []
+        tags_in = []
+        if iteration is not None:
+            ops += [dist.P2POp(dist.isend, self.header(iteration, kind, t), d, self.group) for t, d in s2]
+            for t, s_ in r2:
+                h = self.torch.empty(3, dtype=self.torch.int64, device=self.header(0, 0, t).device)
+                tags_in.append((h, s_))
+                ops.append(dist.P2POp(dist.irecv, h, s_, self.group))
+        ops += [dist.P2POp(dist.isend, t, d, self.group) for t, d in s2]
         ops += [dist.P2POp(dist.irecv, t, s, self.group) for t, s in r2]
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
+        try:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait(timeout=self.timeout)
+        except RuntimeError as e:
+            if "imed out" in str(e) or "imeout" in str(e):
+                raise GridTimeoutError(f"rank {self.rank}: exchange of iteration {iteration} timed out: {e}")
+            raise
+        for h, src in tags_in:
+            it, kd, sr = (int(x) for x in h.cpu().tolist())
+            if it != iteration or kd != kind or sr != src:
+                raise GridProtocolError(f"rank {self.rank} got iteration {it} kind {kd} from rank {sr}, "
+                                        f"expected iteration {iteration} kind {kind} from rank {src}")
         if self.staged:
             for (t, _), (t2, _) in zip(recvs, r2):
                 if t.is_cuda:
@@ -292,7 +322,7 @@ class B200Grid:
             others = [j for j in range(g.c) if j != ci]
             for k, j in enumerate(others):
                 recvs.append((self.inbox[k], self.comm.rank_of(self.i, j)))
-        self.comm.exchange(sends, recvs)
+        self.comm.exchange(sends, recvs, self.iteration, KIND_PARTIAL_SUM)
         for i in range(g.r):  # the reference's accounting, identical on every rank
             log.reduce.messages += g.c - 1
             log.reduce.bytes += (g.c - 1) * self.br * self.byte_width
@@ -330,7 +360,7 @@ class B200Grid:
                 covered[lo - clo:hi - clo] = True
             if not covered.all():
                 raise GridTimeoutError(f"node {(self.i, self.j)}: fragment coverage incomplete")
-            self.comm.exchange(sends, recvs)
+            self.comm.exchange(sends, recvs, self.iteration, KIND_FRAGMENT)
         for i in range(g.r):
             c_i = self.collector_col(i)
             rlo, rhi = self.row_range(i)
