@@ -41,18 +41,24 @@ def _stale():
     return not os.path.exists(LIB) or _newest_dep() > os.path.getmtime(LIB)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, variant=None, defines=()):
+    """Build the library; `variant` + `defines` (-D flags) build an
+    experiment copy into _lib/<variant>/ (loaded with SLD_LIB=<path>)."""
+    lib, obj_dir = LIB, OBJ_DIR
+    if variant:
+        lib = os.path.join(OUT_DIR, variant, "libsldb200.so")
+        obj_dir = os.path.join(OUT_DIR, variant, "obj")
+    elif not force and not _stale():
         return LIB
-    os.makedirs(OBJ_DIR, exist_ok=True)
+    os.makedirs(obj_dir, exist_ok=True)
     cc = nvcc()
     newest = _newest_dep()
 
     def compile_one(src):
-        obj = os.path.join(OBJ_DIR, os.path.splitext(src)[0] + ".o")
-        if not force and os.path.exists(obj) and os.path.getmtime(obj) > newest:
+        obj = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
+        if not force and not variant and os.path.exists(obj) and os.path.getmtime(obj) > newest:
             return obj
-        cmd = [cc, *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [cc, *NVCC_FLAGS, *defines, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
@@ -60,14 +66,18 @@ def build(force=False, verbose=False):
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
         objs = list(pool.map(compile_one, SOURCES))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread", "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    variant = None
+    if "--variant" in sys.argv:
+        variant = sys.argv[sys.argv.index("--variant") + 1]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=variant,
+                defines=[a for a in sys.argv[1:] if a.startswith("-D")]))

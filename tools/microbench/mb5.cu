@@ -55,16 +55,21 @@ __device__ __forceinline__ uint32_t ldg_rec(const uint32_t* p, uint64_t pol){
   return acc;
 }
 
-// MODE 0 ldg, 1 g4, 2 bulk, 3 mix (even warps ldg, odd warps g4)
+// MODE 0 ldg, 1 g4, 2 bulk, 3 mix (even warps ldg, odd warps g4),
+// 4 additivity: warps 0-2 ldg for `iters`, warp 3 g4 for tma_iters
+// (5: warps 0-2 ldg only, warp 3 idle -- the reference for 4)
 template<int ROW, int MODE, int D>
 __global__ void __launch_bounds__(128) kern(const __grid_constant__ CUtensorMap tm, const uint32_t* __restrict__ base,
-                                           uint32_t nrec, uint32_t iters, uint32_t seed, uint32_t* out){
+                                           uint32_t nrec, uint32_t iters, uint32_t seed, uint32_t* out,
+                                           uint32_t tma_iters = 0){
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t tid = blockIdx.x*blockDim.x + threadIdx.x;
   const uint64_t pol = pol_last();
   uint32_t acc = 0;
   const int warp = threadIdx.x >> 5;
-  const bool use_ldg = MODE == 0 || (MODE == 3 && (warp & 1) == 0);
+  const bool use_ldg = MODE == 0 || (MODE == 3 && (warp & 1) == 0) || (MODE >= 4 && warp < 3);
+  if(MODE == 5 && warp == 3) return;
+  if(MODE == 4 && warp == 3) iters = tma_iters;
   if(use_ldg){
     // 4 records per iteration, issued together (as spmv_pass's NB = 4)
     for(uint32_t i=0;i<iters;i++){
@@ -77,8 +82,11 @@ __global__ void __launch_bounds__(128) kern(const __grid_constant__ CUtensorMap 
       acc += v[0]^v[1]^v[2]^v[3];
     }
   } else {
-    uint8_t* ring = sm + (size_t)threadIdx.x * D * (4*ROW);
-    uint64_t* bars = (uint64_t*)(sm + (size_t)blockDim.x * D * (4*ROW)) + threadIdx.x * D;
+    // MODE 4: only warp 3 gathers through TMA and owns the ring
+    const int tix = MODE == 4 ? threadIdx.x - 96 : threadIdx.x;
+    const int nt = MODE == 4 ? 32 : blockDim.x;
+    uint8_t* ring = sm + (size_t)tix * D * (4*ROW);
+    uint64_t* bars = (uint64_t*)(sm + (size_t)nt * D * (4*ROW)) + tix * D;
     auto stage = [&](int s) -> uint8_t* { return ring + s*(4*ROW); };
     auto mb = [&](int s) -> uint64_t* { return bars + s; };
     for(int s=0;s<D;s++) mbar_init(mb(s), 1);
@@ -113,7 +121,8 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 template<int ROW, int MODE, int D>
-int run(const char* name, EncodeFn enc, uint32_t* buf, size_t ws_mb, int ctas_per_sm, int sms, uint32_t* out){
+int run(const char* name, EncodeFn enc, uint32_t* buf, size_t ws_mb, int ctas_per_sm, int sms, uint32_t* out,
+        uint32_t tma_iters = 0){
   const uint32_t nrec = (uint32_t)((ws_mb<<20)/ROW);
   CUtensorMap tm;
   cuuint64_t dims[2] = {ROW/4, nrec};
@@ -124,7 +133,7 @@ int run(const char* name, EncodeFn enc, uint32_t* buf, size_t ws_mb, int ctas_pe
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if(r != CUDA_SUCCESS){ printf("encode failed %d\n", (int)r); return 1; }
   const int thr = 128;
-  const size_t smem = (MODE == 0) ? 0 : (size_t)thr * D * (4*ROW + 8);
+  const size_t smem = (MODE == 0 || MODE == 5) ? 0 : (size_t)(MODE == 4 ? 32 : thr) * D * (4*ROW + 8);
   if(smem > 48*1024) CK(cudaFuncSetAttribute(kern<ROW,MODE,D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int blocks = sms * ctas_per_sm;
   const uint32_t iters = 512;
@@ -132,13 +141,14 @@ int run(const char* name, EncodeFn enc, uint32_t* buf, size_t ws_mb, int ctas_pe
   float best = 1e9;
   for(int rep=0;rep<4;rep++){
     cudaEventRecord(e0);
-    kern<ROW,MODE,D><<<blocks,thr,smem>>>(tm, buf, nrec, iters, rep*77u, out);
+    kern<ROW,MODE,D><<<blocks,thr,smem>>>(tm, buf, nrec, iters, rep*77u, out, tma_iters);
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); CK(cudaGetLastError());
     float ms; cudaEventElapsedTime(&ms,e0,e1); if(rep>0 && ms<best) best=ms;
   }
-  const double recs = (double)blocks*thr*iters*4;
-  printf("%-5s row=%3dB D=%d ctas/SM=%d smem=%6zu ws=%4zu MB: %7.1f G rec/s  %8.1f GB/s  %.3f ms\n",
-         name, ROW, D, ctas_per_sm, smem, ws_mb, recs/best/1e6, recs*ROW/best/1e6, best);
+  double recs = (double)blocks*thr*iters*4;
+  if(MODE >= 4) recs = (double)blocks*96*iters*4 + (MODE == 4 ? (double)blocks*32*tma_iters*4 : 0.0);
+  printf("%-5s row=%3dB D=%d ctas/SM=%d smem=%6zu ws=%4zu MB tma_iters=%4u: %7.1f G rec/s  %8.1f GB/s  %.3f ms\n",
+         name, ROW, D, ctas_per_sm, smem, ws_mb, tma_iters, recs/best/1e6, recs*ROW/best/1e6, best);
   return 0;
 }
 
@@ -151,22 +161,13 @@ int main(){
   EncodeFn enc = (EncodeFn)fn;
   uint32_t* buf; CK(cudaMalloc(&buf,(size_t)1<<30)); CK(cudaMemset(buf,1,(size_t)1<<30));
   uint32_t* out; CK(cudaMalloc(&out,1<<20));
-  for(size_t ws : {32, 58}){
+  // (r02 first run: the ldg / g4 / bulk / mix rates at 32 and 58 MB, profiles/microbench5_tma_r02.txt)
+  for(size_t ws : {32}){
     run<32,0,1>("ldg", enc, buf, ws, 8, sms, out);
-    run<32,1,2>("g4", enc, buf, ws, 4, sms, out);
-    run<32,1,4>("g4", enc, buf, ws, 4, sms, out);
-    run<32,1,4>("g4", enc, buf, ws, 2, sms, out);
-    run<32,1,8>("g4", enc, buf, ws, 2, sms, out);
-    run<32,2,4>("bulk", enc, buf, ws, 4, sms, out);
-    run<32,3,4>("mix", enc, buf, ws, 4, sms, out);
-    run<32,3,4>("mix", enc, buf, ws, 6, sms, out);
-    run<64,0,1>("ldg", enc, buf, ws, 8, sms, out);
-    run<64,1,4>("g4", enc, buf, ws, 2, sms, out);
-    run<64,3,4>("mix", enc, buf, ws, 3, sms, out);
-    run<96,0,1>("ldg", enc, buf, ws, 8, sms, out);
-    run<96,1,4>("g4", enc, buf, ws, 2, sms, out);
-    run<128,0,1>("ldg", enc, buf, ws, 8, sms, out);
-    run<128,1,2>("g4", enc, buf, ws, 2, sms, out);
+    for(int c : {8, 12, 16}){
+      run<32,5,4>("ldg3", enc, buf, ws, c, sms, out, 0);
+      for(uint32_t ti : {32u, 64u, 128u, 256u}) run<32,4,4>("add", enc, buf, ws, c, sms, out, ti);
+    }
   }
   return 0;
 }

@@ -26,20 +26,30 @@ def main():
     ap.add_argument("--frac", default="", help="comma list of SLD_SPLIT_FRAC values")
     ap.add_argument("--bounds", default="", help="semicolon list of SLD_STRIPE_BOUNDS values")
     ap.add_argument("--pf", default="", help="comma list of SLD_PF values (index prefetch distance)")
+    ap.add_argument("--envs", default="", help="semicolon list of K=V[,K=V] environment settings ('none' = none)")
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
     y = _random_residue_limbs(np.random.default_rng(5), A.total_cols, mod)
-    splits = [(sp, fr, pf, bd) for sp in (a.split.split(",") if a.split else [""])
+    splits = [(sp, fr, pf, bd, ev) for sp in (a.split.split(",") if a.split else [""])
               for fr in (a.frac.split(",") if a.frac else [""])
               for pf in (a.pf.split(",") if a.pf else [""])
-              for bd in (a.bounds.split(";") if a.bounds else [""])]
-    for G, (sp, fr, pf, bd) in [(int(x), s) for x in a.chains.split(",") for s in splits]:
+              for bd in (a.bounds.split(";") if a.bounds else [""])
+              for ev in (a.envs.split(";") if a.envs else ["none"])]
+    extra_keys = set()
+    for G, (sp, fr, pf, bd, ev) in [(int(x), s) for x in a.chains.split(",") for s in splits]:
       for k, val in (("SLD_SPLIT", sp), ("SLD_SPLIT_FRAC", fr), ("SLD_PF", pf), ("SLD_STRIPE_BOUNDS", bd)):
           if val:
               os.environ[k] = val
           else:
               os.environ.pop(k, None)
+      for k in extra_keys:
+          os.environ.pop(k, None)
+      if ev and ev != "none":
+          for kv in ev.split(","):
+              k, v = kv.split("=", 1)
+              os.environ[k] = v
+              extra_keys.add(k)
       for sc in [int(x) for x in a.stripes.split(",")]:
         for pol, apw in [(int(x), float(y)) for x in a.policies.split(",") for y in a.apw.split(",")]:
             os.environ["SLD_POLICY"] = str(pol)
@@ -60,7 +70,7 @@ def main():
                                   "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
             inf = dm.info()
             print(f"{a.config} G={G} stripes={inf['stripes']} halves={inf['halves']} split_frac={fr or '-'} "
-                  f"pf={pf or '-'} bounds={bd or '-'} policy={pol} apw={apw}: "
+                  f"pf={pf or '-'} bounds={bd or '-'} env={ev} policy={pol} apw={apw}: "
                   f"{per:.4f} ms/pass = {per / G:.4f} ms per chain-product  [{clk}]",
                   flush=True)
             v.close()
