@@ -402,26 +402,38 @@ def _as_planes(vec, mod):
     return ints_to_planes(vec, digit_count(mod.ell))
 
 
+def _device_list(devices, n):
+    if devices is None:
+        from ._native import device_count
+        devices = list(range(max(1, device_count())))
+    devices = [int(d) for d in devices]
+    if not devices:
+        raise ValueError("empty device list")
+    return devices[:max(1, n)]
+
+
 def krylov_block(A, X, Y, count, muls=None, checkpoint=None, contexts=None,
-                 chains_per_gpu=1) -> BlockSequence:
+                 chains_per_gpu=1, devices=None) -> BlockSequence:
     """a_i = X^T A^i Y with the n column chains independent
     (solver.py:220-257).  Default multipliers are B200Multipliers spread
-    round-robin over the visible devices; chains run on host threads.
-    `chains_per_gpu` = 2 or 4 advances that many chains per matrix pass
-    (B200ChainGroup; unit X, no checkpoint) -- same terms, shared traffic."""
+    round-robin over `devices` (default: every visible GPU); chains run on
+    host threads, one per device slot.  `chains_per_gpu` = 2 or 4 advances
+    that many chains per matrix pass (B200ChainGroup; unit X, no checkpoint)
+    -- same terms, shared traffic."""
     n = len(Y)
     if chains_per_gpu > 1 and muls is None and checkpoint is None and isinstance(X, UnitRows) \
             and n >= chains_per_gpu:
-        return _krylov_block_grouped(A, X, Y, count, chains_per_gpu, contexts)
-    lanes = None  # default multipliers: column j on device j % ndev
+        return _krylov_block_grouped(A, X, Y, count, chains_per_gpu, contexts, devices)
+    lanes = None  # default multipliers: column j on device slot j % ndev
     if muls is None:
-        from ._native import device_count
-        ndev = max(1, min(n, device_count()))
-        # one device matrix per GPU shared by the columns placed on it; the
-        # columns of one GPU run one after another on that GPU's host thread
-        # (a DeviceMatrix, like an sld_ctx, is not shared across threads)
-        shared = [_SharedMatrix(A, d) for d in range(ndev)]
-        muls = [B200Multiplier(A, device=j % ndev, dm=shared[j % ndev]) for j in range(n)]
+        devs = _device_list(devices, n)
+        ndev = len(devs)
+        # one device matrix per device slot shared by the columns placed on
+        # it; the columns of one slot run one after another on that slot's
+        # host thread (a DeviceMatrix, like an sld_ctx, is not shared across
+        # threads)
+        shared = [_SharedMatrix(A, devs[d]) for d in range(ndev)]
+        muls = [B200Multiplier(A, device=devs[j % ndev], dm=shared[j % ndev]) for j in range(n)]
         lanes = [list(range(d, n, ndev)) for d in range(ndev)]
     mod = muls[0].mod
     if contexts is None:
@@ -477,9 +489,9 @@ class _SharedMatrix:
             return self._dm
 
 
-def _krylov_block_grouped(A, X, Y, count, G, contexts):
-    from ._native import device_count
-    ndev = max(1, device_count())
+def _krylov_block_grouped(A, X, Y, count, G, contexts, devices=None):
+    devs = _device_list(devices, len(Y))
+    ndev = len(devs)
     mod = as_modulus(A.mod)
     groups = [list(range(k, min(k + G, len(Y)))) for k in range(0, len(Y), G)]
     if contexts is None:
@@ -491,10 +503,10 @@ def _krylov_block_grouped(A, X, Y, count, G, contexts):
         if len(idx) < G:  # a short last group runs its chains one by one
             res = []
             for j, yp in zip(idx, planes):
-                t, _, _ = krylov_column(B200Multiplier(A, device=gi % ndev), X, yp, count)
+                t, _, _ = krylov_column(B200Multiplier(A, device=devs[gi % ndev]), X, yp, count)
                 res.append(t)
             return res
-        grp = B200ChainGroup(A, chains=G, device=gi % ndev)
+        grp = B200ChainGroup(A, chains=G, device=devs[gi % ndev])
         terms, _ = grp.krylov(X, planes, count)
         return terms
 

@@ -335,3 +335,24 @@ def test_krylov_chain_every_layout(layout, monkeypatch):
     assert planes_to_ints(v) == O.limbs_to_ints(ov)
     if layout == "split":
         assert mul.dm.info()["halves"] == 2
+
+
+@pytest.mark.parametrize("slots", [2, 3])
+def test_krylov_block_multi_device_slots(slots):
+    # krylov_block's multi-GPU placement (round robin over devices, one host
+    # thread and one shared device matrix per slot, solver.py:220-257) with
+    # every slot mapped onto GPU 0: the code path of `slots` GPUs
+    mod = PrimeModulus(2**127 - 1)
+    rng = np.random.default_rng(40 + slots)
+    A = rand_matrix(mod, rng, 120, 120, 9)
+    bp = BlockingParams(5, 7)
+    X, Y = draw_blocks(mod, 120, bp, rng, "unit")
+    ref = krylov_block(A, X, Y, 33, contexts=1, devices=[0])
+    multi = krylov_block(A, X, Y, 33, devices=[0] * slots)
+    grouped = krylov_block(A, X, Y, 33, chains_per_gpu=2, devices=[0] * slots)
+    assert multi.columns == ref.columns == grouped.columns
+    assert multi.spmvs_per_column == [33] * 5
+    orc = to_oracle(A)
+    for j in range(5):
+        ot, _ = O.krylov_unit(orc, O.ints_to_limbs(Y[j], mod.limbs), X.rows, 33)
+        assert multi.columns[j] == [O.limbs_to_ints(t) for t in ot], j
