@@ -39,4 +39,5 @@ def test_repo_arm_two_ranks_folded(config):
     assert d["value"] > 0 and abs(d["value"] - 2 * 40 / (d["ms_per_step"] * 40 / 1e3)) < 1e-6 * d["value"]
     assert d["gpu_launches"] >= 40 and d["witness_check"] is True
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
-    assert d["samples"]["count"] == 20 and d["ms_per_step_median"] > 0
+    # one sample per product pair; per 16 pairs when a product is < 0.1 ms
+    assert d["samples"]["count"] == (2 if config == "cfg1" else 20) and d["ms_per_step_median"] > 0
