@@ -835,7 +835,7 @@ static void mat_free(sld_mat* m) {
   if (!m) return;
   void* ptrs[] = {m->slices, m->pm_idx, m->s_idx, m->s_coef, m->slot_row, m->lane_k4, m->full_ptr,
                   m->full_col, m->full_val, m->dense_val, m->part, m->stage, m->proj_rows,
-                  m->terms_dev, m->dproj_part, m->xch, m->cnt, m->queue, m->mk_y};
+                  m->terms_dev, m->dproj_part, m->xch, m->cnt, m->queue, m->mk_y, m->fix_slots};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->tmp_in) sld_vec_destroy(m->tmp_in);
@@ -907,7 +907,11 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     // gathered vector fits in ~80% of L2 (cfg2 21 MB, cfg5 96 MB), beyond that
     // stripes of <= 1/2 L2 (cfg3: 2 x 58 MB).  With the split, stripes of
     // <= SLD_SPLIT_FRAC (default 0.95) of L2.
-    double frac_one = 0.80, frac_many = 0.5;
+    // Limb-sliced (wide) residues: 2 x 48 MB at cfg5 beats one 96 MB pass
+    // (1.057 vs 1.12 ms, profiles/sweep_cfg5_stripes_r02.txt): the single
+    // pass misses L2 on ~43% of its gathers, and its random DRAM traffic
+    // holds the board at its 1000 W cap (SM clock 1.59 GHz vs 1.96).
+    double frac_one = M->sliced ? 0.55 : 0.80, frac_many = 0.5;
     if (H == 2) {
       frac_one = frac_many = 0.95;
       if (const char* e = getenv("SLD_SPLIT_FRAC")) frac_one = frac_many = atof(e);
@@ -1182,6 +1186,15 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     TRY(dev_upload(&M->dense_val, dense_val, &acct));
     ops(L).to_mont(M->dense_val, (int64_t)M->n_dense * nslots, c->mp, c->stream);
   }
+  if (M->sliced) {
+    // the limb-sliced passes leave full-class entries and dense columns to
+    // full_fixup: the slots that have any
+    std::vector<int32_t> fix;
+    for (int64_t s2 = 0; s2 < nslots; s2++)
+      if (slot_row[s2] >= 0 && (M->n_dense || full_ptr[s2 + 1] > full_ptr[s2])) fix.push_back((int32_t)s2);
+    M->n_fix = (int64_t)fix.size();
+    if (!fix.empty()) TRY(dev_upload(&M->fix_slots, fix, &acct));
+  }
   if (npass > 1) {
     CU(cudaMalloc(&M->part, (size_t)nslots * M->chains * SW * 4));
     acct += (size_t)nslots * M->chains * SW * 4;
@@ -1358,6 +1371,10 @@ void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* p
     }
     if (mk_coeffs && p == M->npass - 1) o.pass_mk(p == 0, M->nslices, c->stream, a, c->mp);
     else o.pass(M->chains, p == 0, p == M->npass - 1, M->nslices, c->stream, a, c->mp);
+  }
+  if (M->sliced && M->n_fix) {
+    a.slices = M->slices;  // (unused by the fixup)
+    o.fixup(a, c->mp, M->fix_slots, M->n_fix, c->stream);
   }
   if (M->apw && c->apw_max) {
     cudaStreamAttrValue v;

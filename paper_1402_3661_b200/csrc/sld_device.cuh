@@ -790,10 +790,34 @@ __global__ void __launch_bounds__(256, SLD_WIDE_MINB) spmv_wide(const SpmvArgs a
 #pragma unroll
     for (int i = 0; i < L; i++) acc2[i] += pin[i];
   }
-  if (LAST && a.has_full) row_full<L, 1>(a, mp, slot, a.slot_row[slot], a.x, acc2);
+  // (full-class entries and dense columns: full_fixup after the last pass --
+  // their Montgomery products inline made every row of the last pass spill)
   uint32_t Rr[L];
   finalize<L>(acc2, 0, mp, Rr);
   store_row<L, 1, LAST>(a, slot, 0, Rr, pol);
+}
+
+// The full-class entries and dense columns of the rows that have them, added
+// to the finished product after the last limb-sliced pass: y[row] <- y[row] +
+// sum f u mod ell (one thread per listed slot; y canonical in biased form)
+template <int L>
+__global__ void __launch_bounds__(128) full_fixup(const SpmvArgs a, const ModParams mp,
+                                                  const int32_t* __restrict__ fix_slots, int64_t nfix) {
+  constexpr int SW = stride_words(L);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nfix) return;
+  const int64_t slot = fix_slots[i];
+  const int32_t row = a.slot_row[slot];
+  if (row < 0) return;
+  const uint32_t* cur = a.npeer ? a.yp[0] + (size_t)(a.peer_off + row) * SW : a.y + (size_t)row * SW;
+  int64_t acc[L + 1];
+#pragma unroll
+  for (int j = 0; j < L; j++) acc[j] = cur[j] ^ 0x80000000u;
+  acc[L] = 0;
+  row_full<L, 1>(a, mp, slot, row, a.x, acc);
+  uint32_t Rr[L];
+  finalize<L>(acc, 0, mp, Rr);
+  store_row<L, 1, true>(a, slot, 0, Rr, 0);
 }
 
 // ------------------------------------------------- die-split SpMV pass

@@ -131,6 +131,8 @@ struct sld_mat {
   uint32_t* part = nullptr;  // slot-indexed partials (npass > 1)
   // limb-sliced passes (one chain, L > 8): T lanes per row, 32 / T rows per slice
   int sliced = 0;
+  int32_t* fix_slots = nullptr;  // sliced: slots with full-class entries (all rows with dense columns)
+  int64_t n_fix = 0;
   // short-row passes (one chain, L <= 8, small N): 4 lanes per row, 8 rows per slice
   int short_rows = 0;
   // die split (halves == 2): each pass's columns are dealt to the two dies

@@ -50,6 +50,9 @@ struct LOps {
   // in its epilogue; slot-order copy of a y vector (false: L > 8)
   bool (*pass_mk)(int first, int64_t nslices, cudaStream_t s, const SpmvArgs& a, const ModParams& mp);
   bool (*mk_gather)(const uint32_t* y, const int32_t* slot_row, int64_t nslots, uint32_t* out, cudaStream_t s);
+  // full-class entries / dense columns of the listed slots, after the last
+  // limb-sliced pass (L > 8)
+  void (*fixup)(const SpmvArgs& a, const ModParams& mp, const int32_t* slots, int64_t n, cudaStream_t s);
 };
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -264,9 +267,12 @@ struct Ops {
     }
     return false;
   }
+  static void fix(const SpmvArgs& a, const ModParams& mp, const int32_t* slots, int64_t n, cudaStream_t s) {
+    if (n) full_fixup<L><<<blocks_for(n, 128), 128, 0, s>>>(a, mp, slots, n);
+  }
   static LOps make() {
     return LOps{pass, split, split_occupancy, shortp, wide, l2s, s2l, mont, zero, dproj, tctx, tcltile, tclapply,
-                tcproj, addm, rrows, lcomb, nz, passmk, mkgather};
+                tcproj, addm, rrows, lcomb, nz, passmk, mkgather, fix};
   }
 };
 
