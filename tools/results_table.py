@@ -1,5 +1,5 @@
-"""Regenerate DESIGN.md §10 (results table) from profiles/bench_*_r01.json:
-python tools/results_table.py [--write]"""
+"""Regenerate DESIGN.md §10 (results table) from profiles/bench_*_r02.json
+(r01 where a config has no r02 run): python tools/results_table.py [--write]"""
 import json
 import os
 import sys
@@ -10,24 +10,34 @@ BEGIN, END = "<!-- results:begin -->", "<!-- results:end -->"
 
 def table():
     rows = []
+    def latest(name):
+        for r in ("r02", "r01"):
+            p = os.path.join(ROOT, "profiles", f"{name}_{r}.json")
+            if os.path.exists(p):
+                return json.loads(open(p).read().strip().splitlines()[-1]), r
+        return None, None
+
     for c in ("cfg1", "cfg2", "cfg3", "cfg5"):
-        p = os.path.join(ROOT, "profiles", f"bench_{c}_r01.json")
-        if not os.path.exists(p):
+        d, r = latest(f"bench_{c}")
+        if d is None:
             continue
-        d = json.loads(open(p).read().strip().splitlines()[-1])
         cpu = (d.get("cpu_baseline") or {}).get("value") or 0.0
-        rows.append(f"| {c} | {d['value']:.0f} | {d.get('ms_per_chain_product', d['ms_per_step']):.4f} | "
-                    f"{d['e2e']['value']:.0f} | {d['roofline']['frac']:.3f} | {d['gather_roofline']['frac']:.2f} "
-                    f"({d['gather_roofline'].get('sectors_per_request', '-')}-sector) | {cpu:.2f} |")
-    ref = os.path.join(ROOT, "profiles", "bench_ref_cfg3_r01.json")
-    refv = json.loads(open(ref).read().strip().splitlines()[-1])["value"] if os.path.exists(ref) else None
+        floor = (d.get("gather_floor") or {}).get("frac_of_floor")
+        rows.append(f"| {c} ({r}) | {d['value']:.0f} | {d.get('ms_per_chain_product', d['ms_per_step']):.4f} | "
+                    f"{d['e2e']['value']:.0f} | {d['roofline']['frac']:.3f} | "
+                    f"{floor if floor is None else f'{floor:.2f}'} | {cpu:.2f} |")
+    ref, _ = latest("bench_ref_cfg3")
     out = [BEGIN,
            "| Config | SpMV/s (device) | ms per chain-product | e2e SpMV/s | HBM roofline frac | "
-           "gather roofline frac | CPU port SpMV/s |",
+           "frac of the gather floor | CPU port SpMV/s |",
            "|---|---|---|---|---|---|---|", *rows, ""]
-    if refv:
+    if ref:
         out.append(f"Reference arm (`bench.py --impl reference`, cfg3, C port of the reference algorithm "
-                   f"on all host cores): {refv:.2f} SpMV/s.")
+                   f"on all host cores): {ref['value']:.2f} SpMV/s.")
+        py = ref.get("reference_python") or {}
+        if py.get("value"):
+            out.append(f"The reference package itself (`sldlag.spmatrix.spmv_planes`, one core) on the same "
+                       f"box: {py['s_per_spmv']:.1f} s per SpMV.")
     out.append(END)
     return "\n".join(out)
 
