@@ -195,6 +195,10 @@ class GridComm:
         except RuntimeError as e:
             if "imed out" in str(e) or "imeout" in str(e):
                 raise GridTimeoutError(f"rank {self.rank}: exchange of iteration {iteration} timed out: {e}")
+            if "onnection closed" in str(e) or "onnection reset" in str(e):
+                # a peer that timed out first tears its connections down: the
+                # message this rank waits for is lost just the same
+                raise GridTimeoutError(f"rank {self.rank}: exchange of iteration {iteration} lost its peer: {e}")
             raise
         for h, src in tags_in:
             it, kd, sr = (int(x) for x in h.cpu().tolist())

@@ -71,7 +71,7 @@ def _worker(rank, world, port, fault, out_q, done):
             res = "timeout: " + str(e)
     except Exception as e:  # report, never hang the parent
         import traceback
-        res = "error: " + traceback.format_exc()
+        res = "error: " + traceback.format_exc()[-1200:]
     out_q.put((rank, res))
     out_q.close()
     out_q.join_thread()  # flush before the hard exit below
