@@ -277,7 +277,7 @@ static int ctx_dies(sld_ctx* c) {
   if (c->die_map) return SLD_OK;
   const DieMap* d = die_map(c->dev, c->sms);
   CU(cudaMalloc(&c->die_map, 256));
-  CU(cudaMemcpy(c->die_map, d->map, 256, cudaMemcpyHostToDevice));
+  CU(h2d(c->die_map, d->map, 256, c->stream));
   if (d->ok) {
     c->die_n[0] = d->n[0];
     c->die_n[1] = d->n[1];
@@ -390,7 +390,7 @@ extern "C" int sld_ctx_create(int device, const uint32_t* ell_limbs, int L, sld_
       for (int b = 0; b < 32; b++) hmod_double(r.data(), mp.ell, L);
     }
     CU(cudaMalloc(&c->fold, tab.size() * 4));
-    CU(cudaMemcpy(c->fold, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+    CU(h2d(c->fold, tab.data(), tab.size() * 4, c->stream));
   }
   *out = c.release();
   return SLD_OK;
@@ -719,7 +719,7 @@ extern "C" int sld_lcset_create(sld_ctx* c, const uint64_t* y_ptrs, int n, int64
   CU(cudaMalloc(&S->Y, std::max<size_t>((size_t)S->mtiles * tcl_ytile_bytes(n), 16)));
   uint64_t* dptrs = nullptr;
   CU(cudaMalloc(&dptrs, 8 * n));
-  CU(cudaMemcpy(dptrs, y_ptrs, 8 * n, cudaMemcpyHostToDevice));
+  CU(h2d(dptrs, y_ptrs, 8 * n, c->stream));
   if (S->mtiles) ops(c->L).tcl_tile((const uint32_t* const*)dptrs, n, rows, S->mtiles, S->Y, c->stream);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   cudaFree(dptrs);
@@ -821,10 +821,10 @@ void parallel_for(int64_t n, F f, int nthreads = 0) {
 }
 
 template <typename T>
-int dev_upload(T** dst, const std::vector<T>& src, size_t* acct) {
+int dev_upload(T** dst, const std::vector<T>& src, size_t* acct, cudaStream_t s) {
   const size_t bytes = std::max<size_t>(src.size() * sizeof(T), 16);
   CU(cudaMalloc(dst, bytes));
-  if (!src.empty()) CU(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  if (!src.empty()) CU(h2d(*dst, src.data(), src.size() * sizeof(T), s));
   *acct += bytes;
   return SLD_OK;
 }
@@ -835,7 +835,7 @@ static void mat_free(sld_mat* m) {
   if (!m) return;
   void* ptrs[] = {m->slices, m->pm_idx, m->s_idx, m->s_coef, m->slot_row, m->lane_k4, m->full_ptr,
                   m->full_col, m->full_val, m->dense_val, m->part, m->stage, m->proj_rows,
-                  m->terms_dev, m->dproj_part, m->xch, m->cnt, m->queue, m->mk_y, m->fix_slots};
+                  m->terms_dev, m->dproj_part, m->xch, m->cnt, m->queue, m->mk_y, m->fix_slots, m->chain_bar};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->tmp_in) sld_vec_destroy(m->tmp_in);
@@ -1048,6 +1048,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
       si.s_k4 = ks;
       pm_units += (uint64_t)kpm * RH;
       s_units += (uint64_t)ks * RH;
+      if (p == 0) M->chain_units = std::max<int64_t>(M->chain_units, (int64_t)(kpm + 2 * ks) * RH);
       if (pm_units >= (1ull << 32) || s_units >= (1ull << 32))
         return fail(SLD_E_BOUND, "matrix too large for 32-bit slice offsets");
     }
@@ -1168,22 +1169,22 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
   // ---- upload
   CU(cudaSetDevice(c->dev));
   size_t acct = 0;
-  TRY(dev_upload(&M->slices, slices, &acct));
+  TRY(dev_upload(&M->slices, slices, &acct, c->stream));
   CU(cudaMalloc(&M->pm_idx, std::max<size_t>(pm_idx.size() * 4, 16)));
-  if (!pm_idx.empty()) CU(cudaMemcpy(M->pm_idx, pm_idx.data(), pm_idx.size() * 4, cudaMemcpyHostToDevice));
+  if (!pm_idx.empty()) CU(h2d(M->pm_idx, pm_idx.data(), pm_idx.size() * 4, c->stream));
   CU(cudaMalloc(&M->s_idx, std::max<size_t>(s_idx.size() * 4, 16)));
-  if (!s_idx.empty()) CU(cudaMemcpy(M->s_idx, s_idx.data(), s_idx.size() * 4, cudaMemcpyHostToDevice));
+  if (!s_idx.empty()) CU(h2d(M->s_idx, s_idx.data(), s_idx.size() * 4, c->stream));
   CU(cudaMalloc(&M->s_coef, std::max<size_t>(s_coef.size() * 4, 16)));
-  if (!s_coef.empty()) CU(cudaMemcpy(M->s_coef, s_coef.data(), s_coef.size() * 4, cudaMemcpyHostToDevice));
+  if (!s_coef.empty()) CU(h2d(M->s_coef, s_coef.data(), s_coef.size() * 4, c->stream));
   acct += pm_idx.size() * 4 + s_idx.size() * 4 + s_coef.size() * 4;
-  TRY(dev_upload(&M->slot_row, slot_row, &acct));
-  TRY(dev_upload(&M->lane_k4, lane_k4, &acct));
-  TRY(dev_upload(&M->full_ptr, full_ptr, &acct));
-  TRY(dev_upload(&M->full_col, full_col, &acct));
-  TRY(dev_upload(&M->full_val, full_val, &acct));
+  TRY(dev_upload(&M->slot_row, slot_row, &acct, c->stream));
+  TRY(dev_upload(&M->lane_k4, lane_k4, &acct, c->stream));
+  TRY(dev_upload(&M->full_ptr, full_ptr, &acct, c->stream));
+  TRY(dev_upload(&M->full_col, full_col, &acct, c->stream));
+  TRY(dev_upload(&M->full_val, full_val, &acct, c->stream));
   if (nf_total) ops(L).to_mont(M->full_val, nf_total, c->mp, c->stream);
   if (M->n_dense) {
-    TRY(dev_upload(&M->dense_val, dense_val, &acct));
+    TRY(dev_upload(&M->dense_val, dense_val, &acct, c->stream));
     ops(L).to_mont(M->dense_val, (int64_t)M->n_dense * nslots, c->mp, c->stream);
   }
   if (M->sliced) {
@@ -1193,7 +1194,7 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     for (int64_t s2 = 0; s2 < nslots; s2++)
       if (slot_row[s2] >= 0 && (M->n_dense || full_ptr[s2 + 1] > full_ptr[s2])) fix.push_back((int32_t)s2);
     M->n_fix = (int64_t)fix.size();
-    if (!fix.empty()) TRY(dev_upload(&M->fix_slots, fix, &acct));
+    if (!fix.empty()) TRY(dev_upload(&M->fix_slots, fix, &acct, c->stream));
   }
   if (npass > 1) {
     CU(cudaMalloc(&M->part, (size_t)nslots * M->chains * SW * 4));
@@ -1203,9 +1204,9 @@ static int mat_build(sld_mat* M, const int64_t* row_ptr, const int32_t* col_idx,
     const size_t xb = (size_t)nslots * M->chains * SW * 4;
     CU(cudaMalloc(&M->xch, xb));
     CU(cudaMalloc(&M->cnt, std::max<size_t>((size_t)nslices * 4, 16)));
-    CU(cudaMemset(M->cnt, 0, std::max<size_t>((size_t)nslices * 4, 16)));
+    CU(cudaMemsetAsync(M->cnt, 0, std::max<size_t>((size_t)nslices * 4, 16), c->stream));
     CU(cudaMalloc(&M->queue, 16));
-    CU(cudaMemset(M->queue, 0, 16));
+    CU(cudaMemsetAsync(M->queue, 0, 16, c->stream));
     acct += xb + (size_t)nslices * 4 + 16;
     int occ = ops(L).split_occupancy(M->chains);
     if (const char* e = getenv("SLD_SPLIT_OCC")) occ = std::max(1, std::min(occ, atoi(e)));
@@ -1258,6 +1259,7 @@ extern "C" int sld_mat_create_chains(sld_ctx* ctx, int chains, int64_t nrows, in
     if (const char* pe = getenv("SLD_SHORT")) sh = atoi(pe) && chains == 1 && ctx->SW <= 8;
     M->short_rows = sh;
   }
+  if (const char* pe = getenv("SLD_CHAIN")) M->chain_ok = atoi(pe) != 0;
   if (const char* pe = getenv("SLD_APW")) M->apw = atoi(pe);
   if (const char* pe = getenv("SLD_APW_RATIO")) M->apw_ratio = (float)atof(pe);
   int r = mat_build(M, row_ptr, col_idx, tags, small_vals, n_full, full_pos, full_limbs, dense_limbs,
@@ -1282,11 +1284,9 @@ extern "C" int sld_mat_info(const sld_mat* m, int64_t* info) {
 
 // ------------------------------------------------------------- SpMV
 
-// launch all stripe passes of one product on the context stream
-void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows,
-                    int proj_m, uint32_t* terms_out, const uint32_t* mk_coeffs) {
-  sld_ctx* c = M->ctx;
-  SpmvArgs a;
+// the arguments every pass of one product shares
+static void product_args(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows, int proj_m,
+                         uint32_t* terms_out, SpmvArgs& a) {
   memset(&a, 0, sizeof(a));
   a.x = x;
   a.y = y;
@@ -1310,6 +1310,14 @@ void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* p
   a.has_full = (M->full_ptr && M->n_full) ? 1 : 0;
   a.policy = M->policy;
   a.pf = (uint32_t)M->pf;
+}
+
+// launch all stripe passes of one product on the context stream
+void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows,
+                    int proj_m, uint32_t* terms_out, const uint32_t* mk_coeffs) {
+  sld_ctx* c = M->ctx;
+  SpmvArgs a;
+  product_args(M, x, y, proj_rows, proj_m, terms_out, a);
   if (!y && M->npeer) {
     a.npeer = M->npeer;
     for (int k = 0; k < M->npeer; k++) a.yp[k] = M->yp[k];
@@ -1382,6 +1390,59 @@ void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* p
     v.accessPolicyWindow.num_bytes = 0;
     cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
   }
+}
+
+// The persistent chain (spmv_chain): small one-pass short-row matrices run
+// many products per launch.  Eligible when the product is that one pass.
+static bool chain_eligible(const sld_mat* M) {
+  return M->chain_ok && M->short_rows && M->npass == 1 && M->halves == 1 && !M->npeer && M->chains == 1 &&
+         M->ctx->L <= 8 && M->nslices > 0 && M->nrows == M->total_cols;
+}
+
+// `steps` products of the chain starting in x (result in x if steps is even,
+// else in y), the projection of product t's input to terms + t * tstride
+static int launch_chain(sld_mat* M, uint32_t* x, uint32_t* y, int64_t steps, const int64_t* proj_rows, int m,
+                        uint32_t* terms, int64_t tstride) {
+  sld_ctx* c = M->ctx;
+  const LOps& o = ops(c->L);
+  static const int env_grid = getenv("SLD_CHAIN_GRID") ? atoi(getenv("SLD_CHAIN_GRID")) : 0;
+  static const int env_mode = getenv("SLD_CHAIN_MODE") ? atoi(getenv("SLD_CHAIN_MODE")) : 0;
+  static const int env_l1 = getenv("SLD_CHAIN_L1") ? atoi(getenv("SLD_CHAIN_L1")) : 1;
+  static const int env_cap = getenv("SLD_CHAIN_CAP") ? atoi(getenv("SLD_CHAIN_CAP")) : 384;
+  // shared-memory staging of each warp's slice: up to env_cap uint4 (6 KB) per warp
+  const uint32_t wcap = (uint32_t)std::min<int64_t>(std::max(env_cap, 0), M->chain_units);
+  const size_t smem = (size_t)8 * wcap * 16;
+  const int occ = o.chain_occupancy(env_l1, smem);
+  if (occ < 1) return fail(SLD_E_CUDA, "persistent chain kernel cannot be resident");
+  if (!M->chain_bar) CU(cudaMalloc(&M->chain_bar, 128));
+  unsigned grid = (unsigned)std::min<int64_t>((int64_t)occ * c->sms, (M->nslices * 32 + 255) / 256);
+  if (env_grid > 0) grid = std::min<unsigned>(grid, (unsigned)env_grid);
+  SpmvArgs a;
+  product_args(M, x, y, proj_rows, m, nullptr, a);
+  a.slices = M->slices;  // the one pass
+  a.lane_k4 = M->lane_k4;
+  a.pf = 0;  // the index streams are L2-resident from the second product on
+  ChainArgs ch;
+  // barrier targets (t + 1) * grid stay below 2^32 per launch
+  const int64_t per = std::max<int64_t>(2, ((int64_t)1 << 31) / grid) & ~(int64_t)1;
+  for (int64_t done = 0; done < steps;) {
+    const int64_t n = std::min(per, steps - done);
+    ch.buf[0] = x;
+    ch.buf[1] = y;
+    ch.bar = M->chain_bar;
+    ch.terms = terms ? terms + (size_t)done * tstride : nullptr;
+    ch.tstride = tstride;
+    ch.steps = n;
+    ch.mode = env_mode;
+    ch.wcap = wcap;
+    a.proj_m = terms ? m : 0;
+    CU(cudaMemsetAsync(M->chain_bar, 0, 4, c->stream));
+    cudaError_t e = o.chain(env_l1, grid, smem, c->stream, a, c->mp, ch);
+    if (e != cudaSuccess) return fail(SLD_E_CUDA, "persistent chain launch: %s", cudaGetErrorString(e));
+    if (n & 1) std::swap(x, y);
+    done += n;
+  }
+  return SLD_OK;
 }
 
 static int spmv_checked(sld_mat* M, sld_vec* in, sld_vec* out, bool sync);
@@ -1553,6 +1614,19 @@ extern "C" int sld_krylov_unit(sld_mat* M, sld_vec* v, const int64_t* x_rows, in
   };
   int rc = SLD_OK;
   int64_t done = 0;
+  if (chain_eligible(M)) {
+    // small matrix: every chunk is one persistent launch
+    while (done < steps && rc == SLD_OK) {
+      const int64_t chunk = std::min<int64_t>(KRYLOV_CHUNK, steps - done);
+      rc = launch_chain(M, v->buf[v->cur], v->buf[v->cur ^ 1], chunk, M->proj_rows, m, m ? area : nullptr,
+                        (int64_t)tstride);
+      if (rc) break;
+      v->cur ^= (int)(chunk & 1);
+      rc = drain_terms(M, area, m, chunk, m ? terms + (size_t)done * m * M->chains * c->L : nullptr, tmp);
+      done += chunk;
+    }
+    return rc;
+  }
   while (done < steps && rc == SLD_OK) {
     const int64_t chunk = std::min<int64_t>(KRYLOV_CHUNK, steps - done);
     int64_t k = 0;
@@ -1615,7 +1689,7 @@ extern "C" int sld_xblock_create(sld_ctx* ctx, const uint32_t* x_limbs, int m, i
       for (int b = 0; b < 32; b++) hmod_double(r.data(), ctx->mp.ell, L);
     }
     CU(cudaMalloc(&xb->fold, tab.size() * 4));
-    CU(cudaMemcpy(xb->fold, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+    CU(h2d(xb->fold, tab.data(), tab.size() * 4, ctx->stream));
     // tensor-core path: m <= 16 terms (32 m byte rows <= 4 M tiles).
     // Measured at cfg3 (tools/bench_dense.py): from m = 4 on it beats the
     // lazy CUDA-core dot products (m = 16: +0.38 vs +0.73 ms per step); at
@@ -1706,6 +1780,41 @@ extern "C" int sld_krylov_dense(sld_mat* M, sld_vec* v, sld_xblock* X, int64_t s
 
 // ------------------------------------------------------------- bench hook
 
+// the bench hook on the persistent chain: one launch per sample of
+// 2 * pairs_per_sample products (even: the iterate returns to its buffer)
+static int bench_chain(sld_mat* M, sld_vec* v, int64_t steps, int warmup, int64_t pairs_per_sample,
+                       double* sample_ms, double* total_ms, double* kernel_ms) {
+  sld_ctx* c = M->ctx;
+  uint32_t *x = v->buf[v->cur], *y = v->buf[v->cur ^ 1];
+  TRY(launch_chain(M, x, y, 2 * std::max<int64_t>(1, (warmup + 1) / 2), nullptr, 0, nullptr, 0));
+  CU(cudaStreamSynchronize(c->stream));
+  const int64_t pairs = (steps + 1) / 2;
+  if (sample_ms && pairs_per_sample < 1) return fail(SLD_E_ARG, "pairs_per_sample must be >= 1");
+  const int64_t per = sample_ms ? pairs_per_sample : pairs;
+  const int64_t nmarks = (pairs + per - 1) / per;
+  std::vector<cudaEvent_t> marks((size_t)nmarks + 1);
+  for (auto& e : marks) CU(cudaEventCreate(&e));
+  CU(cudaEventRecord(marks[0], c->stream));
+  for (int64_t k = 0, j = 1; k < pairs; j++) {
+    const int64_t n = std::min(per, pairs - k);
+    TRY(launch_chain(M, x, y, 2 * n, nullptr, 0, nullptr, 0));
+    CU(cudaEventRecord(marks[(size_t)j], c->stream));
+    k += n;
+  }
+  CU(cudaEventSynchronize(marks.back()));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, marks[0], marks.back()));
+  for (int64_t m = 0; sample_ms && m < nmarks; m++) {
+    float d = 0;
+    CU(cudaEventElapsedTime(&d, marks[(size_t)m], marks[(size_t)m + 1]));
+    sample_ms[m] = d;
+  }
+  for (auto& e : marks) cudaEventDestroy(e);
+  *total_ms = ms;
+  *kernel_ms = ms / (2.0 * pairs);
+  return SLD_OK;
+}
+
 extern "C" int sld_bench_spmv(sld_mat* M, sld_vec* v, int64_t steps, int warmup, double* total_ms,
                               double* kernel_ms) {
   return sld_bench_spmv_samples(M, v, steps, warmup, 0, nullptr, total_ms, kernel_ms);
@@ -1722,6 +1831,7 @@ extern "C" int sld_bench_spmv_samples(sld_mat* M, sld_vec* v, int64_t steps, int
   sld_ctx* c = M->ctx;
   CU(cudaSetDevice(c->dev));
   TRY(vec_alloc_buf(v, v->cur ^ 1));
+  if (chain_eligible(M)) return bench_chain(M, v, steps, warmup, pairs_per_sample, sample_ms, total_ms, kernel_ms);
   // graphs of 2 and 32 products (an even count returns to the same buffer);
   // the long graph amortises launch latency for small matrices
   cudaGraphExec_t ge2 = nullptr, ge32 = nullptr;

@@ -128,6 +128,26 @@ __device__ __forceinline__ void gather_hint(const uint32_t* __restrict__ p, uint
   }
 }
 
+// the same gather through L2 only (.cg): for kernels that read residues other
+// CTAs wrote earlier in the same launch (the persistent chain, spmv_chain),
+// where the non-coherent .nc path may serve a stale line
+template <int SW>
+__device__ __forceinline__ void gather_cg(const uint32_t* __restrict__ p, uint32_t (&u)[SW], uint64_t pol) {
+#pragma unroll
+  for (int q = 0; q < SW / 8; q++) {
+    asm volatile("ld.global.cg.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(u[8 * q + 0]), "=r"(u[8 * q + 1]), "=r"(u[8 * q + 2]), "=r"(u[8 * q + 3]),
+                   "=r"(u[8 * q + 4]), "=r"(u[8 * q + 5]), "=r"(u[8 * q + 6]), "=r"(u[8 * q + 7])
+                 : "l"(p + 8 * q), "l"(pol));
+  }
+}
+
+template <int SW, bool COH>
+__device__ __forceinline__ void gather_x(const uint32_t* __restrict__ p, uint32_t (&u)[SW], uint64_t pol) {
+  if constexpr (COH) gather_cg<SW>(p, u, pol);
+  else gather_hint<SW>(p, u, pol);
+}
+
 template <int SW>
 __device__ __forceinline__ void store_slot_hint(uint32_t* p, const uint32_t (&u)[SW], uint64_t pol) {
 #pragma unroll
@@ -333,7 +353,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 
 // the +-1 and small entries of one row in one part (column stripe [x half]);
 // with K lanes per row (short rows) lane `sub` takes groups sub, sub+K, ...
-template <int L, int G, int K = 1>
+template <int L, int G, int K = 1, bool COH = false>
 __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& si, uint32_t kk, int rw,
                                             const uint32_t* xc, uint64_t pol, uint64_t gpol,
                                             int64_t (&acc)[L + 1], int64_t& S, int sub = 0) {
@@ -355,7 +375,7 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
       uint32_t u[NB][SW];
 #pragma unroll
       for (int e = 0; e < NB; e++)
-        gather_hint<SW>(xc + (size_t)(ws[e0 + e] & 0x7FFFFFFFu) * (G * SW), u[e], gpol);
+        gather_x<SW, COH>(xc + (size_t)(ws[e0 + e] & 0x7FFFFFFFu) * (G * SW), u[e], gpol);
 #pragma unroll
       for (int e = 0; e < NB; e++) {
         const int32_t c = 1 - (int32_t)((ws[e0 + e] >> 30) & 2u);  // +1 / -1
@@ -388,7 +408,7 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
     for (int e0 = 0; e0 < 4; e0 += NB) {
       uint32_t u[NB][SW];
 #pragma unroll
-      for (int e = 0; e < NB; e++) gather_hint<SW>(xc + (size_t)ws[e0 + e] * (G * SW), u[e], gpol);
+      for (int e = 0; e < NB; e++) gather_x<SW, COH>(xc + (size_t)ws[e0 + e] * (G * SW), u[e], gpol);
 #pragma unroll
       for (int e = 0; e < NB; e++) {
         const int32_t c = cs[e0 + e];
@@ -406,14 +426,16 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
 
 // full-class coefficients and dense columns of one row (last pass only):
 // f*u mod ell by Montgomery, f stored as f R
-template <int L, int G>
+template <int L, int G, bool COH = false>
 __device__ __forceinline__ void row_full(const SpmvArgs& a, const ModParams& mp, int64_t slot, int32_t row,
                                          const uint32_t* xc, int64_t (&acc)[L + 1]) {
   constexpr int SW = stride_words(L);
+  const uint64_t npol = COH ? createpolicy_normal() : 0;
 #pragma unroll 1
   for (uint32_t p = a.full_ptr[slot]; p < a.full_ptr[slot + 1]; p++) {
     uint32_t u[SW], f[L], r[L];
-    gather<SW>(xc + (size_t)a.full_col[p] * (G * SW), u);
+    if constexpr (COH) gather_cg<SW>(xc + (size_t)a.full_col[p] * (G * SW), u, npol);
+    else gather<SW>(xc + (size_t)a.full_col[p] * (G * SW), u);
 #pragma unroll
     for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; f[i] = a.full_val[(size_t)p * SW + i]; }
     montmul<L>(f, u, mp, r);
@@ -424,7 +446,8 @@ __device__ __forceinline__ void row_full(const SpmvArgs& a, const ModParams& mp,
 #pragma unroll 1
     for (int g = 0; g < a.n_dense; g++) {
       uint32_t u[SW], f[L], r[L];
-      gather<SW>(xc + (size_t)(a.dense_col0 + g) * (G * SW), u);
+      if constexpr (COH) gather_cg<SW>(xc + (size_t)(a.dense_col0 + g) * (G * SW), u, npol);
+      else gather<SW>(xc + (size_t)(a.dense_col0 + g) * (G * SW), u);
 #pragma unroll
       for (int i = 0; i < L; i++) { u[i] ^= 0x80000000u; }
       // dense values: [g][row], rows padded to nslots
@@ -639,6 +662,199 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const Sp
   uint32_t Rr[L];
   finalize<L>(acc, S, mp, Rr);
   store_row<L, 1, LAST>(a, slot, 0, Rr, pol);
+}
+
+// ------------------------------------------- persistent Krylov chain
+//
+// Small matrices (the short-row layout in one pass) are latency-bound: a
+// product's gathers take ~1.5 us at the request rate, but each warp walks a
+// serial chain of dependent loads (slice table -> group counts -> index group
+// -> gathers -> next index group ...) and the kernel boundary between two
+// products of a CUDA graph adds more.  spmv_chain runs `steps` products of
+// the chain v <- A v in ONE cooperative launch:
+//  * every warp keeps its slice from product to product; the slice's entry
+//    streams are staged in shared memory once (ch.wcap uint4 per warp) and
+//    its table entries stay in registers, so a product's serial chain is
+//    shared-memory index loads and the gathers they feed;
+//  * a grid barrier (one counter, release/acquire at gpu scope) separates
+//    product t from t + 1, and the iterate ping-pongs between two buffers;
+//  * gathers read residues other CTAs wrote in this launch: the barrier's
+//    gpu-scope fences invalidate L1, so within a product the iterate can be
+//    cached in L1 (L1G, hot columns) or read through L2 only (.cg).
+// The unit-X projection of each input iterate goes to terms + t * tstride.
+struct ChainArgs {
+  uint32_t* buf[2];  // buf[0] holds the input iterate; product t reads buf[t & 1]
+  uint32_t* bar;     // barrier counter, zero at launch
+  uint32_t* terms;   // projection of product t's input at terms + t * tstride
+  int64_t tstride;   // words
+  int64_t steps;
+  uint32_t wcap;     // shared-memory entry-stream capacity per warp (uint4)
+  int mode;          // experiments (env SLD_CHAIN_MODE): bit0 skips the products (barrier cost alone)
+};
+
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t target) {
+  __syncthreads();  // this CTA's stores of the product are issued
+  if (threadIdx.x == 0) {
+    __threadfence();  // ... and visible at gpu scope before the arrival
+    atomicAdd(bar, 1u);
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+template <int SW, bool L1G>
+__device__ __forceinline__ void chain_gather(const uint32_t* p, uint32_t (&u)[SW], uint64_t pol) {
+  if constexpr (L1G) {
+#pragma unroll
+    for (int q = 0; q < SW / 8; q++)
+      asm volatile("ld.global.ca.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                   : "=r"(u[8 * q + 0]), "=r"(u[8 * q + 1]), "=r"(u[8 * q + 2]), "=r"(u[8 * q + 3]),
+                     "=r"(u[8 * q + 4]), "=r"(u[8 * q + 5]), "=r"(u[8 * q + 6]), "=r"(u[8 * q + 7])
+                   : "l"(p + 8 * q), "l"(pol));
+  } else {
+    gather_cg<SW>(p, u, pol);
+  }
+}
+
+// one row's +-1 and small entries, K = SHORT_K lanes per row (lane `sub`
+// takes groups sub, sub + K, ...); pm / sx / sc point at the row's group 0
+// in shared memory (staged slice) or global memory, group stride R
+template <int L, bool L1G>
+__device__ __forceinline__ void chain_entries(const uint4* pm, const uint4* sx, const int4* sc, uint32_t kk,
+                                              int sub, const uint32_t* x, uint64_t gpol, int64_t (&acc)[L + 1],
+                                              int64_t& S) {
+  constexpr int SW = stride_words(L);
+  constexpr int R = 32 / SHORT_K;
+  const uint32_t my_pm = kk & 0xFFFFu, my_s = kk >> 16;
+#pragma unroll 1
+  for (uint32_t k = sub; k < my_pm; k += SHORT_K) {
+    const uint4 w = pm[(size_t)k * R];
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint32_t u[4][SW];
+#pragma unroll
+    for (int e = 0; e < 4; e++) chain_gather<SW, L1G>(x + (size_t)(ws[e] & 0x7FFFFFFFu) * SW, u[e], gpol);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int32_t c = 1 - (int32_t)((ws[e] >> 30) & 2u);
+      S += c;
+#pragma unroll
+      for (int i = 0; i < L; i++) acc[i] += (int64_t)c * (int64_t)(int32_t)u[e][i];
+    }
+  }
+#pragma unroll 1
+  for (uint32_t k = sub; k < my_s; k += SHORT_K) {
+    const uint4 w = sx[(size_t)k * R];
+    const int4 cf = sc[(size_t)k * R];
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    const int32_t cs[4] = {cf.x, cf.y, cf.z, cf.w};
+    uint32_t u[4][SW];
+#pragma unroll
+    for (int e = 0; e < 4; e++) chain_gather<SW, L1G>(x + (size_t)ws[e] * SW, u[e], gpol);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      S += cs[e];
+#pragma unroll
+      for (int i = 0; i < L; i++) {
+        const int64_t p = (int64_t)cs[e] * (int64_t)(int32_t)u[e][i];
+        acc[i] += (int64_t)(uint32_t)p;
+        acc[i + 1] += (int64_t)(int32_t)(p >> 32);
+      }
+    }
+  }
+}
+
+template <int L, bool L1G>
+__global__ void __launch_bounds__(256, 3) spmv_chain(const SpmvArgs a, const ModParams mp, const ChainArgs ch) {
+  extern __shared__ uint4 chain_smem[];
+  constexpr int SW = stride_words(L);
+  constexpr int R = 32 / SHORT_K;
+  const int lane = threadIdx.x & 31;
+  const int rw = lane / SHORT_K, sub = lane % SHORT_K;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // the whole matrix and both iterates stay L2-resident from product to product
+  const uint64_t pol = createpolicy_normal();
+  const uint64_t gpol = policy_evict_last();
+  // this warp's first slice: table entries in registers, entry streams
+  // staged in shared memory when they fit the warp's share
+  uint4* wsm = chain_smem + (size_t)(threadIdx.x >> 5) * ch.wcap;
+  SliceInfo si0{0, 0, 0, 0};
+  uint32_t kk0 = 0;
+  int32_t row0 = -1;
+  bool staged = false;
+  if (warp0 < a.nslices) {
+    si0 = a.slices[warp0];
+    kk0 = a.lane_k4[warp0 * R + rw];
+    row0 = a.slot_row[warp0 * R + rw];
+    const uint32_t npm = si0.pm_k4 * R, ns = si0.s_k4 * R;
+    staged = npm + 2 * ns <= ch.wcap;
+    if (staged) {
+      for (uint32_t i = lane; i < npm; i += 32) wsm[i] = a.pm_idx[si0.pm_off + i];
+      for (uint32_t i = lane; i < ns; i += 32) {
+        wsm[npm + i] = a.s_idx[si0.s_off + i];
+        const int4 c = a.s_coef[si0.s_off + i];
+        wsm[npm + ns + i] = make_uint4((uint32_t)c.x, (uint32_t)c.y, (uint32_t)c.z, (uint32_t)c.w);
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll 1
+  for (int64_t t = 0; t < ch.steps; t++) {
+    const uint32_t* x = (t & 1) ? ch.buf[1] : ch.buf[0];
+    uint32_t* y = (t & 1) ? ch.buf[0] : ch.buf[1];
+    if (blockIdx.x == 0 && threadIdx.x < a.proj_m) {
+      uint32_t u[SW];
+      gather_cg<SW>(x + (size_t)a.proj_rows[threadIdx.x] * SW, u, pol);
+      uint32_t* dst = ch.terms + (size_t)t * ch.tstride + (size_t)threadIdx.x * SW;
+#pragma unroll
+      for (int i = 0; i < SW; i++) dst[i] = i < L ? (u[i] ^ 0x80000000u) : 0u;
+    }
+#pragma unroll 1
+    for (int64_t slice = warp0; slice < ((ch.mode & 1) ? 0 : a.nslices); slice += nwarps) {
+      const bool first = slice == warp0;
+      const int64_t slot = slice * R + rw;
+      const SliceInfo si = first ? si0 : a.slices[slice];
+      const uint32_t kk = first ? kk0 : a.lane_k4[slot];
+      const int32_t row = first ? row0 : a.slot_row[slot];
+      const uint4 *pm, *sx;
+      const int4* sc;
+      if (first && staged) {
+        pm = wsm + rw;
+        sx = wsm + si.pm_k4 * R + rw;
+        sc = reinterpret_cast<const int4*>(wsm + (si.pm_k4 + si.s_k4) * R) + rw;
+      } else {
+        pm = a.pm_idx + si.pm_off + rw;
+        sx = a.s_idx + si.s_off + rw;
+        sc = a.s_coef + si.s_off + rw;
+      }
+      int64_t acc[L + 1];
+#pragma unroll
+      for (int i = 0; i <= L; i++) acc[i] = 0;
+      int64_t S = 0;
+      chain_entries<L, L1G>(pm, sx, sc, kk, sub, x, gpol, acc, S);
+#pragma unroll
+      for (int off = 1; off < SHORT_K; off <<= 1) {
+#pragma unroll
+        for (int i = 0; i <= L; i++) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+        S += __shfl_xor_sync(0xffffffffu, S, off);
+      }
+      if (sub == 0) {
+        if (a.has_full) row_full<L, 1, true>(a, mp, slot, row, x, acc);
+        uint32_t Rr[L];
+        finalize<L>(acc, S, mp, Rr);
+        if (row >= 0) {
+          uint32_t o[SW];
+#pragma unroll
+          for (int i = 0; i < SW; i++) o[i] = i < L ? (Rr[i] ^ 0x80000000u) : 0u;
+          store_slot<SW>(y + (size_t)row * SW, o);
+        }
+      }
+    }
+    if (t + 1 < ch.steps) grid_barrier(ch.bar, (uint32_t)(t + 1) * gridDim.x);
+  }
 }
 
 // ------------------------------------------------ limb-sliced SpMV pass

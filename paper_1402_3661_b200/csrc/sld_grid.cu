@@ -333,7 +333,8 @@ extern "C" int sld_grid_create(sld_mat* M, int r, int c, int rank, int64_t n_pad
   g->lay = layout_of(g->br, g->bc, c, g->c->SW);
   cudaError_t e = cudaSetDevice(g->c->dev);
   if (e == cudaSuccess) e = cudaMalloc(&g->mem, g->lay.bytes);
-  if (e == cudaSuccess) e = cudaMemset(g->mem, 0, g->lay.bytes);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->mem, 0, g->lay.bytes, g->c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->c->stream);
   if (e != cudaSuccess) {
     if (g->mem) cudaFree(g->mem);
     delete g;
@@ -445,10 +446,10 @@ extern "C" int sld_grid_set_projection(sld_grid* g, const int64_t* rows, int m, 
   }
   if (owned) std::memcpy(owned, g->owned.data(), (size_t)m);
   CU(cudaMalloc(&g->rows_dev, (size_t)m * 8));
-  CU(cudaMemcpy(g->rows_dev, loc.data(), (size_t)m * 8, cudaMemcpyHostToDevice));
+  CU(h2d(g->rows_dev, loc.data(), (size_t)m * 8, g->c->stream));
   CU(cudaMalloc(&g->terms, (size_t)max_steps * m * g->c->SW * 4));
   CU(cudaMalloc(&g->counter, 4));
-  CU(cudaMemset(g->counter, 0, 4));
+  CU(cudaMemsetAsync(g->counter, 0, 4, g->c->stream));
   g->m = m;
   g->cap = max_steps;
   g->recorded = 0;
@@ -543,7 +544,7 @@ extern "C" int sld_grid_terms(sld_grid* g, uint32_t* out, int64_t* steps) {
           out[(s * g->m + t) * c->L + w] =
               g->owned[(size_t)t] ? raw[(s * g->m + t) * c->SW + w] ^ 0x80000000u : 0u;
   }
-  CU(cudaMemset(g->counter, 0, 4));
+  CU(cudaMemsetAsync(g->counter, 0, 4, c->stream));
   *steps = n;
   g->recorded = 0;
   return SLD_OK;
@@ -560,7 +561,7 @@ extern "C" int sld_grid_set_epoch(sld_grid* g, int64_t epoch) {
   h.epoch = e;
   h.flag = e * (uint32_t)g->nodes;
   for (int k = 0; k < MAXN; k++) h.peer_epoch[k] = e;
-  CU(cudaMemcpy(g->ctl, &h, sizeof(h), cudaMemcpyHostToDevice));
+  CU(h2d(g->ctl, &h, sizeof(h), g->c->stream));
   g->iteration = epoch;
   return SLD_OK;
 }

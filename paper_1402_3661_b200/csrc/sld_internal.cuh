@@ -61,6 +61,16 @@ struct sld_ctx {
 };
 
 void ctx_free(sld_ctx* c);
+// host -> device copy ordered on `s` and complete on return.  A plain
+// cudaMemcpy from pageable memory may return before its DMA has landed, and
+// the context streams are non-blocking: a kernel queued right after it (a
+// Montgomery conversion, the first product) could read the old bytes.
+inline cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return e;
+}
+
 inline void ctx_unref(sld_ctx* c) {
   if (c && c->refs.fetch_sub(1) == 1) ctx_free(c);
 }
@@ -135,6 +145,9 @@ struct sld_mat {
   int64_t n_fix = 0;
   // short-row passes (one chain, L <= 8, small N): 4 lanes per row, 8 rows per slice
   int short_rows = 0;
+  int chain_ok = 1;                 // persistent chain kernel allowed (env SLD_CHAIN=0 disables)
+  uint32_t* chain_bar = nullptr;    // its grid-barrier counter
+  int64_t chain_units = 0;          // largest slice's entry streams (uint4), pass 0
   // die split (halves == 2): each pass's columns are dealt to the two dies
   int halves = 1;
   // peer push (set by the grid, sld_grid.cu): the last pass stores into these buffers

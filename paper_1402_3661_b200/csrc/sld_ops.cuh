@@ -53,6 +53,11 @@ struct LOps {
   // full-class entries / dense columns of the listed slots, after the last
   // limb-sliced pass (L > 8)
   void (*fixup)(const SpmvArgs& a, const ModParams& mp, const int32_t* slots, int64_t n, cudaStream_t s);
+  // persistent chain of short-row products (L <= 8): resident CTAs per SM
+  // (0: unsupported), and the cooperative launch of `grid` CTAs
+  int (*chain_occupancy)(int l1g, size_t smem);
+  cudaError_t (*chain)(int l1g, unsigned grid, size_t smem, cudaStream_t s, const SpmvArgs& a, const ModParams& mp,
+                       const ChainArgs& ch);
 };
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -270,9 +275,31 @@ struct Ops {
   static void fix(const SpmvArgs& a, const ModParams& mp, const int32_t* slots, int64_t n, cudaStream_t s) {
     if (n) full_fixup<L><<<blocks_for(n, 128), 128, 0, s>>>(a, mp, slots, n);
   }
+  static int chain_occ(int l1g, size_t smem) {
+    if constexpr (L <= 8) {
+      const void* f = l1g ? (const void*)spmv_chain<L, true> : (const void*)spmv_chain<L, false>;
+      if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+      int n = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, 256, smem) != cudaSuccess) return 0;
+      return n;
+    }
+    return 0;
+  }
+  static cudaError_t chainl(int l1g, unsigned grid, size_t smem, cudaStream_t s, const SpmvArgs& a,
+                            const ModParams& mp, const ChainArgs& ch) {
+    if constexpr (L <= 8) {
+      SpmvArgs a2 = a;
+      ModParams mp2 = mp;
+      ChainArgs ch2 = ch;
+      void* args[] = {&a2, &mp2, &ch2};
+      const void* f = l1g ? (const void*)spmv_chain<L, true> : (const void*)spmv_chain<L, false>;
+      return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(256), args, smem, s);
+    }
+    return cudaErrorNotSupported;
+  }
   static LOps make() {
     return LOps{pass, split, split_occupancy, shortp, wide, l2s, s2l, mont, zero, dproj, tctx, tcltile, tclapply,
-                tcproj, addm, rrows, lcomb, nz, passmk, mkgather, fix};
+                tcproj, addm, rrows, lcomb, nz, passmk, mkgather, fix, chain_occ, chainl};
   }
 };
 

@@ -356,3 +356,27 @@ def test_krylov_block_multi_device_slots(slots):
     for j in range(5):
         ot, _ = O.krylov_unit(orc, O.ints_to_limbs(Y[j], mod.limbs), X.rows, 33)
         assert multi.columns[j] == [O.limbs_to_ints(t) for t in ot], j
+
+
+@pytest.mark.parametrize("chain", ["1", "0"])
+@pytest.mark.parametrize("bits,n,steps", [(31, 500, 37), (160, 2000, 1030), (202, 60000, 21), (256, 3000, 65)])
+def test_persistent_chain_vs_oracle(chain, bits, n, steps, monkeypatch):
+    # small one-pass matrices run many products per cooperative launch
+    # (spmv_chain, grid barrier between products); SLD_CHAIN=0 forces the
+    # per-product graphs.  n = 60000 leaves several slices per warp.
+    monkeypatch.setenv("SLD_CHAIN", chain)
+    from paper_1402_3661_b200 import corpus
+    mod = corpus.random_prime(bits, np.random.default_rng(bits))
+    rng = np.random.default_rng(n)
+    if n > 5000:
+        A = corpus.generate(corpus.CorpusProfile(n=n, gamma=20, dense_cols=1, seed=3), mod)
+    else:
+        A = rand_matrix(mod, rng, n, n - 1, 20, dense=1, full_frac=0.02)
+    y = mod.random_residues(rng, n)
+    rows = [0, n // 2, n - 1]
+    ot, ov = O.krylov_unit(to_oracle(A), O.ints_to_limbs(y, mod.limbs), rows, steps)
+    mul = B200Multiplier(A)
+    terms, v, spmvs = krylov_column(mul, UnitRows(rows), ints_to_planes(y, digit_count(mod.ell)), steps)
+    assert spmvs == steps
+    assert terms == [O.limbs_to_ints(t) for t in ot]
+    assert planes_to_ints(v) == O.limbs_to_ints(ov)
