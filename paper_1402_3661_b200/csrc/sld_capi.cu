@@ -1393,7 +1393,11 @@ void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* p
 }
 
 // The persistent chain (spmv_chain): small one-pass short-row matrices run
-// many products per launch.  Eligible when the product is that one pass.
+// many products per launch.  Opt-in (SLD_CHAIN=1): measured on B200 it is
+// slower than the per-product graphs (cfg1 7.0 vs 6.0 us per product) -- its
+// grid barrier costs 1.3-1.6 us (2+ us with >400 CTAs), as much as the kernel
+// boundary it removes, and a product's gathers are bound by the per-SM
+// request rate, not by the launch (profiles/chain_cfg1_r02.txt).
 static bool chain_eligible(const sld_mat* M) {
   return M->chain_ok && M->short_rows && M->npass == 1 && M->halves == 1 && !M->npeer && M->chains == 1 &&
          M->ctx->L <= 8 && M->nslices > 0 && M->nrows == M->total_cols;
@@ -1411,11 +1415,13 @@ static int launch_chain(sld_mat* M, uint32_t* x, uint32_t* y, int64_t steps, con
   static const int env_cap = getenv("SLD_CHAIN_CAP") ? atoi(getenv("SLD_CHAIN_CAP")) : 384;
   // shared-memory staging of each warp's slice: up to env_cap uint4 (6 KB) per warp
   const uint32_t wcap = (uint32_t)std::min<int64_t>(std::max(env_cap, 0), M->chain_units);
-  const size_t smem = (size_t)8 * wcap * 16;
-  const int occ = o.chain_occupancy(env_l1, smem);
+  static const int tb = getenv("SLD_CHAIN_TB") ? atoi(getenv("SLD_CHAIN_TB")) : 64;
+  const size_t smem = (size_t)(tb / 32) * wcap * 16;
+  const int occ = o.chain_occupancy(env_l1, tb, smem);
   if (occ < 1) return fail(SLD_E_CUDA, "persistent chain kernel cannot be resident");
   if (!M->chain_bar) CU(cudaMalloc(&M->chain_bar, 128));
-  unsigned grid = (unsigned)std::min<int64_t>((int64_t)occ * c->sms, (M->nslices * 32 + 255) / 256);
+  // small CTAs spread the slices evenly over the SMs
+  unsigned grid = (unsigned)std::min<int64_t>((int64_t)occ * c->sms, (M->nslices * 32 + tb - 1) / tb);
   if (env_grid > 0) grid = std::min<unsigned>(grid, (unsigned)env_grid);
   SpmvArgs a;
   product_args(M, x, y, proj_rows, m, nullptr, a);
@@ -1435,9 +1441,8 @@ static int launch_chain(sld_mat* M, uint32_t* x, uint32_t* y, int64_t steps, con
     ch.steps = n;
     ch.mode = env_mode;
     ch.wcap = wcap;
-    a.proj_m = terms ? m : 0;
     CU(cudaMemsetAsync(M->chain_bar, 0, 4, c->stream));
-    cudaError_t e = o.chain(env_l1, grid, smem, c->stream, a, c->mp, ch);
+    cudaError_t e = o.chain(env_l1, grid, tb, smem, c->stream, a, c->mp, ch);
     if (e != cudaSuccess) return fail(SLD_E_CUDA, "persistent chain launch: %s", cudaGetErrorString(e));
     if (n & 1) std::swap(x, y);
     done += n;

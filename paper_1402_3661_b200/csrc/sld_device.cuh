@@ -389,13 +389,16 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
   // into its low word (limb i) and signed high word (limb i+1)
   const uint4* sp = a.s_idx + si.s_off + rw;
   const int4* cp = a.s_coef + si.s_off + rw;
+  // with K lanes per row, small group 0 goes to the lane after the one that
+  // took the last +-1 group, so the row's groups spread evenly over its lanes
+  const uint32_t s0 = K > 1 ? (uint32_t)(sub + K - (int)(my_pm % K)) % K : 0u;
 #pragma unroll 1
-  for (uint32_t k = sub; k < PF && k < my_s; k += K) {
+  for (uint32_t k = s0; k < PF && k < my_s; k += K) {
     prefetch_l2(sp + (size_t)k * R);
     prefetch_l2(cp + (size_t)k * R);
   }
 #pragma unroll 1
-  for (uint32_t k = sub; k < my_s; k += K) {
+  for (uint32_t k = s0; k < my_s; k += K) {
     if (PF && k + PF < my_s) {
       prefetch_l2(sp + (size_t)(k + PF) * R);
       prefetch_l2(cp + (size_t)(k + PF) * R);
@@ -645,6 +648,15 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const Sp
   for (int i = 0; i <= L; i++) acc[i] = 0;
   int64_t S = 0;
   row_entries<L, 1, SHORT_K>(a, si, kk, rw, a.x, pol, gpol, acc, S, sub);
+  // the partial and the full-class entries go into other lanes' sums before
+  // the reduction, so their loads overlap instead of trailing the row's tail
+  if (!FIRST && sub == 2) {
+    uint32_t pin[SW];
+    load_slot<SW>(a.part_in + (size_t)slot * SW, pin, pol);
+#pragma unroll
+    for (int i = 0; i < L; i++) acc[i] += pin[i];
+  }
+  if (LAST && a.has_full && sub == SHORT_K - 1) row_full<L, 1>(a, mp, slot, a.slot_row[slot], a.x, acc);
 #pragma unroll
   for (int off = 1; off < SHORT_K; off <<= 1) {
 #pragma unroll
@@ -652,13 +664,6 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const Sp
     S += __shfl_xor_sync(0xffffffffu, S, off);
   }
   if (sub != 0) return;
-  if (!FIRST) {
-    uint32_t pin[SW];
-    load_slot<SW>(a.part_in + (size_t)slot * SW, pin, pol);
-#pragma unroll
-    for (int i = 0; i < L; i++) acc[i] += pin[i];
-  }
-  if (LAST && a.has_full) row_full<L, 1>(a, mp, slot, a.slot_row[slot], a.x, acc);
   uint32_t Rr[L];
   finalize<L>(acc, S, mp, Rr);
   store_row<L, 1, LAST>(a, slot, 0, Rr, pol);
@@ -689,18 +694,23 @@ struct ChainArgs {
   int64_t tstride;   // words
   int64_t steps;
   uint32_t wcap;     // shared-memory entry-stream capacity per warp (uint4)
-  int mode;          // experiments (env SLD_CHAIN_MODE): bit0 skips the products (barrier cost alone)
+  int mode;          // experiments (env SLD_CHAIN_MODE, wrong results): bit0 skips the products (the
+                     // barrier alone), bit1 the reductions, bit2 the full-class entries, bit3 the ping-pong
 };
 
+// CTA-wide arrive (release: cumulative over the CTA's stores, which bar.sync
+// ordered before it) and wait.  The poll is relaxed and one acquire fence
+// follows it: an acquire load per poll would invalidate the SM's L1 on every
+// spin (CCTL.IVALL), under the CTAs still computing on the same SM.
 __device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t target) {
-  __syncthreads();  // this CTA's stores of the product are issued
+  __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();  // ... and visible at gpu scope before the arrival
-    atomicAdd(bar, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     uint32_t v;
     do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
     } while (v < target);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }
@@ -744,8 +754,9 @@ __device__ __forceinline__ void chain_entries(const uint4* pm, const uint4* sx, 
       for (int i = 0; i < L; i++) acc[i] += (int64_t)c * (int64_t)(int32_t)u[e][i];
     }
   }
+  const uint32_t s0 = (uint32_t)(sub + SHORT_K - (int)(my_pm % SHORT_K)) % SHORT_K;  // as in row_entries
 #pragma unroll 1
-  for (uint32_t k = sub; k < my_s; k += SHORT_K) {
+  for (uint32_t k = s0; k < my_s; k += SHORT_K) {
     const uint4 w = sx[(size_t)k * R];
     const int4 cf = sc[(size_t)k * R];
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
@@ -803,8 +814,9 @@ __global__ void __launch_bounds__(256, 3) spmv_chain(const SpmvArgs a, const Mod
   }
 #pragma unroll 1
   for (int64_t t = 0; t < ch.steps; t++) {
-    const uint32_t* x = (t & 1) ? ch.buf[1] : ch.buf[0];
-    uint32_t* y = (t & 1) ? ch.buf[0] : ch.buf[1];
+    const bool odd = (t & 1) && !(ch.mode & 8);  // mode bit 3 (experiment): always buf[0] -> buf[1]
+    const uint32_t* x = odd ? ch.buf[1] : ch.buf[0];
+    uint32_t* y = odd ? ch.buf[0] : ch.buf[1];
     if (blockIdx.x == 0 && threadIdx.x < a.proj_m) {
       uint32_t u[SW];
       gather_cg<SW>(x + (size_t)a.proj_rows[threadIdx.x] * SW, u, pol);
@@ -835,6 +847,8 @@ __global__ void __launch_bounds__(256, 3) spmv_chain(const SpmvArgs a, const Mod
       for (int i = 0; i <= L; i++) acc[i] = 0;
       int64_t S = 0;
       chain_entries<L, L1G>(pm, sx, sc, kk, sub, x, gpol, acc, S);
+      // full-class entries in the row's last lane, before the reduction
+      if (a.has_full && !(ch.mode & 4) && sub == SHORT_K - 1) row_full<L, 1, true>(a, mp, slot, row, x, acc);
 #pragma unroll
       for (int off = 1; off < SHORT_K; off <<= 1) {
 #pragma unroll
@@ -842,9 +856,13 @@ __global__ void __launch_bounds__(256, 3) spmv_chain(const SpmvArgs a, const Mod
         S += __shfl_xor_sync(0xffffffffu, S, off);
       }
       if (sub == 0) {
-        if (a.has_full) row_full<L, 1, true>(a, mp, slot, row, x, acc);
         uint32_t Rr[L];
-        finalize<L>(acc, S, mp, Rr);
+        if (ch.mode & 2) {  // experiment: no reduction (wrong results)
+#pragma unroll
+          for (int i = 0; i < L; i++) Rr[i] = (uint32_t)acc[i] ^ (uint32_t)S;
+        } else {
+          finalize<L>(acc, S, mp, Rr);
+        }
         if (row >= 0) {
           uint32_t o[SW];
 #pragma unroll

@@ -145,7 +145,7 @@ struct sld_mat {
   int64_t n_fix = 0;
   // short-row passes (one chain, L <= 8, small N): 4 lanes per row, 8 rows per slice
   int short_rows = 0;
-  int chain_ok = 1;                 // persistent chain kernel allowed (env SLD_CHAIN=0 disables)
+  int chain_ok = 0;                 // persistent chain kernel (opt-in, env SLD_CHAIN=1): measured slower
   uint32_t* chain_bar = nullptr;    // its grid-barrier counter
   int64_t chain_units = 0;          // largest slice's entry streams (uint4), pass 0
   // die split (halves == 2): each pass's columns are dealt to the two dies

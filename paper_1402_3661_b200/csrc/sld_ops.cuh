@@ -55,10 +55,12 @@ struct LOps {
   void (*fixup)(const SpmvArgs& a, const ModParams& mp, const int32_t* slots, int64_t n, cudaStream_t s);
   // persistent chain of short-row products (L <= 8): resident CTAs per SM
   // (0: unsupported), and the cooperative launch of `grid` CTAs
-  int (*chain_occupancy)(int l1g, size_t smem);
-  cudaError_t (*chain)(int l1g, unsigned grid, size_t smem, cudaStream_t s, const SpmvArgs& a, const ModParams& mp,
-                       const ChainArgs& ch);
+  int (*chain_occupancy)(int l1g, int tb, size_t smem);
+  cudaError_t (*chain)(int l1g, unsigned grid, int tb, size_t smem, cudaStream_t s, const SpmvArgs& a,
+                       const ModParams& mp, const ChainArgs& ch);
 };
+
+constexpr int SHORT_TB = 64;  // threads per CTA of the short-row pass (env SLD_SHORT_TB)
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
@@ -163,12 +165,15 @@ struct Ops {
   static bool shortp(int first, int last, int64_t nslices, cudaStream_t s, const SpmvArgs& a,
                      const ModParams& mp) {
     if constexpr (L <= 8) {
-      const unsigned grid = blocks_for(nslices * 32, 256);
+      // small CTAs spread the few slices of a small matrix evenly over the SMs
+      // (each SM gathers ~1 residue per clock)
+      static const int tb = getenv("SLD_SHORT_TB") ? atoi(getenv("SLD_SHORT_TB")) : SHORT_TB;
+      const unsigned grid = blocks_for(nslices * 32, tb);
       if (!grid) return true;
-      if (first && last) spmv_short<L, true, true><<<grid, 256, 0, s>>>(a, mp);
-      else if (first) spmv_short<L, true, false><<<grid, 256, 0, s>>>(a, mp);
-      else if (last) spmv_short<L, false, true><<<grid, 256, 0, s>>>(a, mp);
-      else spmv_short<L, false, false><<<grid, 256, 0, s>>>(a, mp);
+      if (first && last) spmv_short<L, true, true><<<grid, tb, 0, s>>>(a, mp);
+      else if (first) spmv_short<L, true, false><<<grid, tb, 0, s>>>(a, mp);
+      else if (last) spmv_short<L, false, true><<<grid, tb, 0, s>>>(a, mp);
+      else spmv_short<L, false, false><<<grid, tb, 0, s>>>(a, mp);
       return true;
     }
     return false;
@@ -275,17 +280,17 @@ struct Ops {
   static void fix(const SpmvArgs& a, const ModParams& mp, const int32_t* slots, int64_t n, cudaStream_t s) {
     if (n) full_fixup<L><<<blocks_for(n, 128), 128, 0, s>>>(a, mp, slots, n);
   }
-  static int chain_occ(int l1g, size_t smem) {
+  static int chain_occ(int l1g, int tb, size_t smem) {
     if constexpr (L <= 8) {
       const void* f = l1g ? (const void*)spmv_chain<L, true> : (const void*)spmv_chain<L, false>;
       if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
       int n = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, 256, smem) != cudaSuccess) return 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, tb, smem) != cudaSuccess) return 0;
       return n;
     }
     return 0;
   }
-  static cudaError_t chainl(int l1g, unsigned grid, size_t smem, cudaStream_t s, const SpmvArgs& a,
+  static cudaError_t chainl(int l1g, unsigned grid, int tb, size_t smem, cudaStream_t s, const SpmvArgs& a,
                             const ModParams& mp, const ChainArgs& ch) {
     if constexpr (L <= 8) {
       SpmvArgs a2 = a;
@@ -293,7 +298,7 @@ struct Ops {
       ChainArgs ch2 = ch;
       void* args[] = {&a2, &mp2, &ch2};
       const void* f = l1g ? (const void*)spmv_chain<L, true> : (const void*)spmv_chain<L, false>;
-      return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(256), args, smem, s);
+      return cudaLaunchCooperativeKernel(f, dim3(grid), dim3(tb), args, smem, s);
     }
     return cudaErrorNotSupported;
   }
