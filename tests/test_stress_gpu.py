@@ -58,3 +58,39 @@ def test_fresh_builds_first_product():
         dm.spmv(vi, vo)
         assert np.array_equal(vo.download_limbs(), want)
         dm.close()
+
+
+@pytest.mark.parametrize("it", range(10))
+def test_random_layouts_vs_oracle(it):
+    # the other layouts on fresh builds: one lane per row (spmv_pass, above
+    # the short-row size), 1-3 column stripes, chain groups of 2, and the
+    # limb-sliced wide kernel with its full-class fixup (> 256-bit moduli)
+    from paper_1402_3661_b200 import B200ChainGroup
+    rng = np.random.default_rng(2000 + it)
+    bits = int(rng.choice([61, 202, 256, 300, 420, 650]))
+    n = int(rng.integers(80000, 140000))
+    steps = int(rng.integers(4, 14))
+    stripes = int(rng.integers(1, 4))
+    mod = corpus.random_prime(bits, np.random.default_rng(bits))
+    A = corpus.generate(corpus.CorpusProfile(n=n, gamma=int(rng.integers(10, 30)),
+                                             dense_cols=int(rng.integers(0, 2)), seed=50 + it), mod)
+    stripe_cols = 0 if stripes == 1 else -(-A.total_cols // stripes)
+    G = 2 if (bits <= 512 and it % 2 == 0) else 1
+    ys = [mod.random_residues(rng, n) for _ in range(G)]
+    rows = [0, int(rng.integers(1, n)), n - 1]
+    orc = to_oracle(A)
+    P = digit_count(mod.ell)
+    if G == 1:
+        mul = B200Multiplier(A, stripe_cols=stripe_cols)
+        terms, v, _ = krylov_column(mul, UnitRows(rows), ints_to_planes(ys[0], P), steps)
+        got, gv = [terms], [planes_to_ints(v)]
+    else:
+        grp = B200ChainGroup(A, chains=G, stripe_cols=stripe_cols)
+        got, vs = grp.krylov(UnitRows(rows), [ints_to_planes(y, P) for y in ys], steps)
+        gv = [planes_to_ints(v) for v in vs]
+    for g in range(G):
+        ot, ov = O.krylov_unit(orc, O.ints_to_limbs(ys[g], mod.limbs), rows, steps)
+        want = [O.limbs_to_ints(t) for t in ot]
+        ctx = (it, bits, n, stripes, G, g)
+        assert got[g] == want, (ctx, [(k, j) for k in range(steps) for j in range(3) if got[g][k][j] != want[k][j]][:5])
+        assert gv[g] == O.limbs_to_ints(ov), ctx
