@@ -163,6 +163,15 @@ int sld_lincomb(sld_ctx *ctx, const uint64_t *y_ptrs, const uint32_t *coeffs, in
 typedef struct sld_lcset sld_lcset;
 int sld_lcset_create(sld_ctx *ctx, const uint64_t *y_ptrs, int n, int64_t rows, sld_lcset **out);
 int sld_lcset_apply(sld_lcset *s, const uint32_t *coeffs, uint64_t acc_ptr, uint64_t dst_ptr);
+/* The combinations of K = 2 or 4 Horner steps in one pass over the tiled y
+ * (the y are fixed for a Mksol run, only the coefficients change): dst_k =
+ * sum_s coeffs[k][s] y_s mod ell, coeffs K x n x L canonical limbs,
+ * dst_ptrs[k] device vectors of `rows` residues.  Asynchronous. */
+int sld_lcset_apply_batch(sld_lcset *s, const uint32_t *coeffs, int K, const uint64_t *dst_ptrs);
+/* The set tiled in matrix m's slot order (one chain, pass layout): its
+ * combinations are slot-ordered vectors of nslots residues, the addv operand
+ * of sld_spmv_add. */
+int sld_lcset_create_slots(sld_mat *m, const uint64_t *y_ptrs, int n, sld_lcset **out);
 int sld_lcset_destroy(sld_lcset *s);
 
 /* *out = 1 if any residue of v is non-zero (np.any(planes), solver.py:545). */
@@ -219,6 +228,12 @@ int sld_krylov_dense(sld_mat *m, sld_vec *v, sld_xblock *x, int64_t steps, uint3
  */
 int sld_mat_mksol_bind(sld_mat *m, sld_vec *const *ys, int n);
 int sld_spmv_mksol(sld_mat *m, sld_vec *in, sld_vec *out, const uint32_t *coeffs);
+/* The Horner step with its combination precomputed (sld_lcset_apply_batch):
+ * out = A in + addv (mod l), the addition in the last pass's epilogue
+ * (the reference's planes_add_mod, vecops.py:270-278); addv in m's slot
+ * order (sld_lcset_create_slots), nslots residues.  L <= 8, one chain,
+ * pass or short-row layout (SLD_E_ARG otherwise).  Asynchronous. */
+int sld_spmv_add(sld_mat *m, sld_vec *in, sld_vec *out, sld_vec *addv);
 
 /*
  * Timing hook for bench.py: runs `steps` products v <- A v on device

@@ -34,12 +34,12 @@ EXPORTS = [
     "sld_vec_create", "sld_vec_create_chains", "sld_vec_destroy", "sld_vec_upload_planes", "sld_vec_download_planes",
     "sld_vec_upload_limbs", "sld_vec_download_limbs", "sld_vec_device_ptr",
     "sld_vec_upload_planes_chains", "sld_vec_download_planes_chains",
-    "sld_lcset_create", "sld_lcset_apply", "sld_lcset_destroy",
+    "sld_lcset_create", "sld_lcset_apply", "sld_lcset_apply_batch", "sld_lcset_create_slots", "sld_lcset_destroy",
     "sld_spmv", "sld_spmv_async", "sld_spmv_planes", "sld_krylov_unit",
     "sld_xblock_create", "sld_xblock_destroy", "sld_krylov_dense",
     "sld_bench_spmv", "sld_bench_spmv_samples", "sld_corpus_rows", "sld_corpus_fill",
     "sld_sldm_info", "sld_sldm_read", "sld_sldm_write", "sld_sldv_write", "sld_sldv_info", "sld_sldv_read",
-    "sld_split_block", "sld_mat_mksol_bind", "sld_spmv_mksol",
+    "sld_split_block", "sld_mat_mksol_bind", "sld_spmv_mksol", "sld_spmv_add",
     "sld_grid_create", "sld_grid_blob", "sld_grid_connect", "sld_grid_set_timeout", "sld_grid_set_projection",
     "sld_grid_load", "sld_grid_read", "sld_grid_launch", "sld_grid_wait", "sld_grid_iterate", "sld_grid_terms",
     "sld_grid_set_epoch", "sld_grid_info", "sld_grid_destroy",
@@ -111,6 +111,8 @@ def load(build_if_missing=False):
             "sld_vec_upload_planes_chains": ([vp, vp, i64, i32], i32),
             "sld_lcset_create": ([vp, vp, i32, i64, pp], i32),
             "sld_lcset_apply": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64], i32),
+            "sld_lcset_apply_batch": ([vp, vp, i32, vp], i32),
+            "sld_lcset_create_slots": ([vp, vp, i32, vp], i32),
             "sld_lcset_destroy": ([vp], i32),
             "sld_vec_download_planes_chains": ([vp, vp, i64, i32], i32),
             "sld_vec_download_limbs": ([vp, vp, i64], i32),
@@ -136,6 +138,7 @@ def load(build_if_missing=False):
                                  vp, vp, vp, vp, i32], i32),
             "sld_mat_mksol_bind": ([vp, vp, i32], i32),
             "sld_spmv_mksol": ([vp, vp, vp, vp], i32),
+            "sld_spmv_add": ([vp, vp, vp, vp], i32),
             "sld_grid_create": ([vp, i32, i32, i32, i64, vp], i32),
             "sld_grid_blob": ([vp, vp], i32),
             "sld_grid_connect": ([vp, vp], i32),

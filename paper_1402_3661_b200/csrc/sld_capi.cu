@@ -705,7 +705,23 @@ struct sld_lcset {
   uint8_t* Y = nullptr;    // [mtiles][n][...] canonical K-major tiles
 };
 
+static int lcset_create(sld_ctx* c, const uint64_t* y_ptrs, int n, int64_t rows, const int32_t* perm,
+                        sld_lcset** out);
+
 extern "C" int sld_lcset_create(sld_ctx* c, const uint64_t* y_ptrs, int n, int64_t rows, sld_lcset** out) {
+  return lcset_create(c, y_ptrs, n, rows, nullptr, out);
+}
+
+// the same set tiled in a matrix's slot order: its combinations come out
+// slot-ordered (nslots residues), the operand sld_spmv_add reads coalesced
+extern "C" int sld_lcset_create_slots(sld_mat* M, const uint64_t* y_ptrs, int n, sld_lcset** out) {
+  if (!M) return fail(SLD_E_ARG, "null matrix");
+  if (M->chains != 1 || M->halves != 1 || M->sliced) return fail(SLD_E_ARG, "slot-ordered set needs a pass layout");
+  return lcset_create(M->ctx, y_ptrs, n, M->nslots, M->slot_row, out);
+}
+
+static int lcset_create(sld_ctx* c, const uint64_t* y_ptrs, int n, int64_t rows, const int32_t* perm,
+                        sld_lcset** out) {
   if (!c || !out || n < 1 || n > 8 || rows < 0 || !y_ptrs) return fail(SLD_E_ARG, "bad combination set");
   if (c->L > 8) return fail(SLD_E_ARG, "tensor-core combination needs ell < 2^256");
   CU(cudaSetDevice(c->dev));
@@ -720,7 +736,7 @@ extern "C" int sld_lcset_create(sld_ctx* c, const uint64_t* y_ptrs, int n, int64
   uint64_t* dptrs = nullptr;
   CU(cudaMalloc(&dptrs, 8 * n));
   CU(h2d(dptrs, y_ptrs, 8 * n, c->stream));
-  if (S->mtiles) ops(c->L).tcl_tile((const uint32_t* const*)dptrs, n, rows, S->mtiles, S->Y, c->stream);
+  if (S->mtiles) ops(c->L).tcl_tile((const uint32_t* const*)dptrs, n, rows, S->mtiles, S->Y, perm, c->stream);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   cudaFree(dptrs);
   if (e != cudaSuccess) return fail(SLD_E_CUDA, "combination set: %s", cudaGetErrorString(e));
@@ -751,6 +767,24 @@ extern "C" int sld_lcset_apply(sld_lcset* S, const uint32_t* coeffs, uint64_t ac
   if (S->mtiles)
     ops(L).tcl_apply(S->Y, cf, S->n, S->rows, S->mtiles, S->grid, (const uint32_t*)(uintptr_t)acc_ptr,
                      (uint32_t*)(uintptr_t)dst_ptr, c->fold, c->mp, c->stream);
+  CU(cudaGetLastError());
+  return SLD_OK;
+}
+
+// the combinations of K (2 or 4) Horner steps in one pass over the tiled y:
+// dst_k = sum_s coeffs[k][s] y_s mod ell (coeffs: K x n x L limbs,
+// canonical).  Asynchronous on the context stream.
+extern "C" int sld_lcset_apply_batch(sld_lcset* S, const uint32_t* coeffs, int K, const uint64_t* dst_ptrs) {
+  if (!S || !coeffs || !dst_ptrs || (K != 2 && K != 4)) return fail(SLD_E_ARG, "bad batched combination");
+  sld_ctx* c = S->ctx;
+  CU(cudaSetDevice(c->dev));
+  uint32_t* d[TCL_KMAX];
+  for (int k = 0; k < K; k++) {
+    if (!dst_ptrs[k]) return fail(SLD_E_ARG, "null output");
+    d[k] = (uint32_t*)(uintptr_t)dst_ptrs[k];
+  }
+  if (!ops(c->L).tcl_batch(K, S->Y, coeffs, S->n, S->rows, S->mtiles, c->sms, d, c->fold, c->mp, c->stream))
+    return fail(SLD_E_ARG, "batched combination needs ell < 2^256");
   CU(cudaGetLastError());
   return SLD_OK;
 }
@@ -1314,10 +1348,11 @@ static void product_args(sld_mat* M, const uint32_t* x, uint32_t* y, const int64
 
 // launch all stripe passes of one product on the context stream
 void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows,
-                    int proj_m, uint32_t* terms_out, const uint32_t* mk_coeffs) {
+                    int proj_m, uint32_t* terms_out, const uint32_t* mk_coeffs, const uint32_t* addv) {
   sld_ctx* c = M->ctx;
   SpmvArgs a;
   product_args(M, x, y, proj_rows, proj_m, terms_out, a);
+  a.addv = addv;
   if (!y && M->npeer) {
     a.npeer = M->npeer;
     for (int k = 0; k < M->npeer; k++) a.yp[k] = M->yp[k];
@@ -1515,6 +1550,25 @@ extern "C" int sld_spmv_mksol(sld_mat* M, sld_vec* in, sld_vec* out, const uint3
     return fail(SLD_E_ARG, "bad Mksol step vectors");
   CU(cudaSetDevice(M->ctx->dev));
   launch_product(M, in->buf[in->cur], out->buf[out->cur], nullptr, 0, nullptr, coeffs);
+  CU(cudaGetLastError());
+  return SLD_OK;
+}
+
+// Mksol Horner step with the combination precomputed (sld_lcset_apply_batch
+// on a slot-ordered set): out = A in + addv mod ell, addv in the matrix's
+// slot order (read coalesced by the last pass's epilogue).  One
+// chain, L <= 8, pass or short-row layouts (not limb-sliced, not die-split).
+extern "C" int sld_spmv_add(sld_mat* M, sld_vec* in, sld_vec* out, sld_vec* addv) {
+  if (!M || !in || !out || !addv) return fail(SLD_E_ARG, "null argument");
+  sld_ctx* c = M->ctx;
+  if (c->L > 8 || M->chains != 1 || M->halves != 1 || M->sliced || M->npeer)
+    return fail(SLD_E_ARG, "the fused addition needs one chain, ell < 2^256 and a pass layout");
+  if (in->n != M->total_cols || out->n < M->nrows || addv->n < M->nslots || in == out || addv == out)
+    return fail(SLD_E_ARG, "vector shapes do not match the matrix");
+  if (addv->ctx != c || in->ctx != c || out->ctx != c) return fail(SLD_E_ARG, "context mismatch");
+  CU(cudaSetDevice(c->dev));
+  TRY(vec_alloc_buf(out, out->cur));
+  launch_product(M, in->buf[in->cur], out->buf[out->cur], nullptr, 0, nullptr, nullptr, addv->buf[addv->cur]);
   CU(cudaGetLastError());
   return SLD_OK;
 }

@@ -81,7 +81,11 @@ struct SpmvArgs {
   const uint32_t* fold;  // 2^(32k) mod ell for k = L .. 2L, L words each
   int mk_n;
   uint32_t mk_c[8][8];  // the step's coefficients, canonical, L limbs each
+  // Mksol Horner step with a precomputed combination (last pass, one chain,
+  // L <= 8): the output row becomes (A w)[row] + addv[row] mod ell
+  const uint32_t* addv;  // row-indexed biased vector, or null
 };
+
 
 // ---------------------------------------------------------------- loads
 
@@ -427,6 +431,19 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
   }
 }
 
+// add the precomputed combination addv[slot] (slot-ordered, so a warp's
+// loads are coalesced) into a row's sums before its Barrett reduction (one
+// more canonical term: the bounds of finalize hold)
+template <int L>
+__device__ __forceinline__ void add_slot_vector(const SpmvArgs& a, int64_t slot, uint64_t pol,
+                                                int64_t (&acc)[L + 1]) {
+  constexpr int SW = stride_words(L);
+  uint32_t u[SW];
+  load_slot<SW>(a.addv + (size_t)slot * SW, u, pol);
+#pragma unroll
+  for (int i = 0; i < L; i++) acc[i] += (int64_t)(u[i] ^ 0x80000000u);
+}
+
 // full-class coefficients and dense columns of one row (last pass only):
 // f*u mod ell by Montgomery, f stored as f R
 template <int L, int G, bool COH = false>
@@ -597,6 +614,7 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
     for (int i = 0; i < L; i++) acc[i] += pin[i];
   }
   if (LAST && a.has_full) row_full<L, G>(a, mp, slot, a.slot_row[slot], xc, acc);
+  if (G == 1 && LAST && a.addv) add_slot_vector<L>(a, slot, pol, acc);
   uint32_t Rr[L];
   finalize<L>(acc, S, mp, Rr);
   if constexpr (MK) mk_combine<L>(a, slot, mp, pol, Rr);
@@ -657,6 +675,7 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const Sp
     for (int i = 0; i < L; i++) acc[i] += pin[i];
   }
   if (LAST && a.has_full && sub == SHORT_K - 1) row_full<L, 1>(a, mp, slot, a.slot_row[slot], a.x, acc);
+  if (LAST && a.addv && sub == 1) add_slot_vector<L>(a, slot, pol, acc);
 #pragma unroll
   for (int off = 1; off < SHORT_K; off <<= 1) {
 #pragma unroll

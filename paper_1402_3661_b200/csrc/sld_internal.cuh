@@ -184,4 +184,4 @@ const sld::LOps& ops(int L);
 // y == nullptr and peers set (the grid, sld_grid.cu) the last pass stores into
 // the peers' buffers.  proj_rows / terms_out: fused unit-X projection of x.
 void launch_product(sld_mat* M, const uint32_t* x, uint32_t* y, const int64_t* proj_rows, int proj_m,
-                    uint32_t* terms_out, const uint32_t* mk_coeffs = nullptr);
+                    uint32_t* terms_out, const uint32_t* mk_coeffs = nullptr, const uint32_t* addv = nullptr);

@@ -4,6 +4,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstring>
+
 #include "sld_dense.cuh"
 #include "sld_device.cuh"
 #include "sld_tcgemm.cuh"
@@ -36,9 +39,13 @@ struct LOps {
   // digit GEMM, fold.  False when L > 8.
   bool (*tc_tile_x)(const uint32_t* x, int m, int64_t n, int MT, int64_t ktiles, uint8_t* A, cudaStream_t s);
   // tensor-core Mksol combination (L <= 8, n <= 8): tile the y set once, combine per step
-  bool (*tcl_tile)(const uint32_t* const* ys_dev, int n, int64_t rows, int64_t mtiles, uint8_t* Y, cudaStream_t s);
+  bool (*tcl_tile)(const uint32_t* const* ys_dev, int n, int64_t rows, int64_t mtiles, uint8_t* Y,
+                   const int32_t* perm, cudaStream_t s);
   bool (*tcl_apply)(const uint8_t* Y, const TclCoef& cf, int n, int64_t rows, int64_t mtiles, int grid,
                     const uint32_t* acc, uint32_t* dst, const uint32_t* fold, const ModParams& mp, cudaStream_t s);
+  // K (2 or 4) Horner steps' combinations in one pass over the tiled y set
+  bool (*tcl_batch)(int K, const uint8_t* Y, const uint32_t* coefs, int n, int64_t rows, int64_t mtiles, int sms,
+                    uint32_t* const* dsts, const uint32_t* fold, const ModParams& mp, cudaStream_t s);
   bool (*tc_project)(const uint32_t* v, int64_t n, int m, int MT, int64_t ktiles, const uint8_t* A, uint8_t* B,
                      uint32_t* partial, int nct, int64_t kt_per_cta, const uint32_t* fold, const ModParams& mp,
                      uint32_t* out, cudaStream_t s);
@@ -213,10 +220,11 @@ struct Ops {
     }
     return false;
   }
-  static bool tcltile(const uint32_t* const* ys, int n, int64_t rows, int64_t mtiles, uint8_t* Y, cudaStream_t s) {
+  static bool tcltile(const uint32_t* const* ys, int n, int64_t rows, int64_t mtiles, uint8_t* Y, const int32_t* perm,
+                      cudaStream_t s) {
     if constexpr (L <= 8) {
       const int64_t cores = mtiles * n * 32;
-      tcl_tile_y<L><<<blocks_for(cores, 128), 128, 0, s>>>(ys, n, rows, mtiles, Y);
+      tcl_tile_y<L><<<blocks_for(cores, 128), 128, 0, s>>>(ys, n, rows, mtiles, Y, perm);
       return true;
     }
     return false;
@@ -226,12 +234,45 @@ struct Ops {
                        cudaStream_t s) {
     if constexpr (L <= 8) {
       static bool attr = [] {
-        cudaFuncSetAttribute(tcl_combine<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl_smem_bytes(8));
+        cudaFuncSetAttribute(tcl_combine<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl_smem_bytes(8));
         return true;
       }();
       (void)attr;
-      tcl_combine<L><<<grid, TCL_THREADS, tcl_smem_bytes(n), s>>>(Y, cf, n, rows, mtiles, acc, dst, fold, mp);
+      TclBatch<1> b;
+      memcpy(b.w[0], cf.w, sizeof(cf.w));
+      b.dst[0] = dst;
+      tcl_combine<L, 1><<<grid, TCL_THREADS, tcl_smem_bytes(n), s>>>(Y, b, n, rows, mtiles, acc, fold, mp);
       return true;
+    }
+    return false;
+  }
+  template <int K>
+  static bool tclbatch_k(const uint8_t* Y, const uint32_t* coefs, int n, int64_t rows, int64_t mtiles, int sms,
+                         uint32_t* const* dsts, const uint32_t* fold, const ModParams& mp, cudaStream_t s) {
+    static const int occ = [] {
+      cudaFuncSetAttribute(tcl_combine<L, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcl_smem_bytes(8, K));
+      int o = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tcl_combine<L, K>, tcl_threads(K), tcl_smem_bytes(8, K));
+      return std::max(1, o);
+    }();
+    TclBatch<K> b;
+    memset(&b, 0, sizeof(b));
+    for (int k = 0; k < K; k++) {
+      for (int j = 0; j < n; j++)
+        for (int i = 0; i < L; i++) b.w[k][j][i] = coefs[((size_t)k * n + j) * L + i];
+      b.dst[k] = dsts[k];
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, (int64_t)occ * sms));
+    tcl_combine<L, K><<<grid, tcl_threads(K), tcl_smem_bytes(n, K), s>>>(Y, b, n, rows, mtiles, nullptr, fold, mp);
+    return true;
+  }
+  // K in {2, 4} steps' combinations in one pass over Y' (coefs: [K][n][L] canonical)
+  static bool tclbatch(int K, const uint8_t* Y, const uint32_t* coefs, int n, int64_t rows, int64_t mtiles,
+                       int sms, uint32_t* const* dsts, const uint32_t* fold, const ModParams& mp, cudaStream_t s) {
+    if constexpr (L <= 8) {
+      if (!mtiles) return true;
+      if (K == 2) return tclbatch_k<2>(Y, coefs, n, rows, mtiles, sms, dsts, fold, mp, s);
+      if (K == 4) return tclbatch_k<4>(Y, coefs, n, rows, mtiles, sms, dsts, fold, mp, s);
     }
     return false;
   }
@@ -304,7 +345,7 @@ struct Ops {
   }
   static LOps make() {
     return LOps{pass, split, split_occupancy, shortp, wide, l2s, s2l, mont, zero, dproj, tctx, tcltile, tclapply,
-                tcproj, addm, rrows, lcomb, nz, passmk, mkgather, fix, chain_occ, chainl};
+                tclbatch, tcproj, addm, rrows, lcomb, nz, passmk, mkgather, fix, chain_occ, chainl};
   }
 };
 

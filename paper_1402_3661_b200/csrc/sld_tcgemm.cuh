@@ -330,25 +330,43 @@ __global__ void __launch_bounds__(1024) tc_proj_final(const uint32_t* __restrict
 // 2^(32k) mod ell, adds acc, and runs finalize: w is written once, never
 // staged.  Y' (the n fixed vectors) is tiled once per Mksol run; C'
 // (n x 2 KB) is expanded in shared memory from the step's coefficients.
+//
+// Batched (K > 1): the combinations of K Horner steps at once.  The y are
+// fixed for the whole Mksol run and only the coefficients change per step,
+// so one pass over Y' (n x 115 MB at cfg3, the dominant traffic) feeds K
+// accumulators: K C' tiles in shared memory, K x 64 TMEM columns per
+// buffer, K outputs per tile.  Per step the traffic drops from
+// (n + 2) vectors to n / K + 1.
 constexpr int TCL_N = 64;                       // byte positions k of the products
 constexpr uint32_t TCL_IDESC = (2u << 4) | ((uint32_t)(TCL_N >> 3) << 17) | ((128u >> 4) << 24);
-constexpr int TCL_STAGES = 3;
 constexpr int TCL_THREADS = 192;
+// epilogue warps per TMEM lane quarter: the batched kernel's K reductions
+// per row are split over two warps of each quarter (more epilogue warps per
+// SM: it runs one CTA per SM)
+__host__ __device__ constexpr int tcl_epi(int K) { return K == 1 ? 1 : (K == 2 ? 2 : 4); }
+__host__ __device__ constexpr int tcl_threads(int K) { return 64 + 128 * tcl_epi(K); }
 #ifndef TCL_CTAS_PER_SM
 #define TCL_CTAS_PER_SM 2  // two CTAs per SM: twice the epilogue warps (smem 2 x ~113 KB, TMEM 2 x 128 cols)
 #endif
+constexpr int TCL_KMAX = 4;  // Horner steps per batched combination
 
+// Y' pipeline stages: 3 for one step, 2 when K C' tiles share the smem
+__host__ __device__ constexpr int tcl_stages(int K) { return K == 1 ? 3 : 2; }
 __host__ __device__ constexpr int tcl_ytile_bytes(int n) { return 128 * 32 * n; }
 __host__ __device__ constexpr int tcl_b_bytes(int n) { return TCL_N * 32 * n; }
-__host__ __device__ constexpr int tcl_smem_bytes(int n) {
-  return TCL_STAGES * tcl_ytile_bytes(n) + tcl_b_bytes(n) + 1024;
+__host__ __device__ constexpr int tcl_smem_bytes(int n, int K = 1) {
+  return tcl_stages(K) * tcl_ytile_bytes(n) + K * tcl_b_bytes(n) + 1024;
 }
+// TMEM columns: two accumulator buffers of K x 64 columns (a power of 2 >= 32)
+__host__ __device__ constexpr uint32_t tcl_tmem_cols(int K) { return K == 1 ? 128u : (K == 2 ? 256u : 512u); }
 
 // y_s (biased slots) -> Y' tiles: tile mt = [s][mg][kc][8 rows][16 bytes];
 // one thread per 128-byte core matrix (the 16 bytes of a row are 4 limb words)
+// perm (optional): tile row i holds row perm[i] of the y (-1: zero), so the
+// combinations come out in a matrix's slot order
 template <int L>
 __global__ void tcl_tile_y(const uint32_t* const* __restrict__ ys, int n, int64_t rows, int64_t mtiles,
-                           uint8_t* __restrict__ Y) {
+                           uint8_t* __restrict__ Y, const int32_t* __restrict__ perm) {
   constexpr int SW = stride_words(L);
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t per_tile = (int64_t)n * 32;
@@ -359,11 +377,12 @@ __global__ void tcl_tile_y(const uint32_t* const* __restrict__ ys, int n, int64_
   uint32_t o[32];
 #pragma unroll
   for (int rr = 0; rr < 8; rr++) {
-    const int64_t i = mt * 128 + mg * 8 + rr;
+    const int64_t i0 = mt * 128 + mg * 8 + rr;
+    const int64_t i = (perm && i0 < rows) ? (int64_t)perm[i0] : i0;
 #pragma unroll
     for (int w = 0; w < 4; w++) {
       const int limb = kc * 4 + w;
-      o[rr * 4 + w] = (i < rows && limb < L) ? (ys[s][(size_t)i * SW + limb] ^ 0x80000000u) : 0u;
+      o[rr * 4 + w] = (i0 < rows && i >= 0 && limb < L) ? (ys[s][(size_t)i * SW + limb] ^ 0x80000000u) : 0u;
     }
   }
   uint4* dst = reinterpret_cast<uint4*>(Y + (size_t)idx * 128);
@@ -378,18 +397,27 @@ struct TclCoef {
   uint32_t w[8][8];  // [s][limb], canonical
 };
 
-template <int L>
-__global__ void __launch_bounds__(TCL_THREADS, TCL_CTAS_PER_SM)
-    tcl_combine(const uint8_t* __restrict__ Y, const TclCoef cf, int n, int64_t rows,
-                int64_t mtiles, const uint32_t* __restrict__ acc, uint32_t* __restrict__ dst,
-                const uint32_t* __restrict__ fold, const ModParams mp) {
+// K steps' coefficients and outputs of one batched combination
+template <int K>
+struct TclBatch {
+  uint32_t w[K][8][8];  // [step][s][limb], canonical
+  uint32_t* dst[K];     // row-indexed outputs (biased slots)
+};
+
+template <int L, int K>
+__global__ void __launch_bounds__(tcl_threads(K), K == 1 ? TCL_CTAS_PER_SM : 1)
+    tcl_combine(const uint8_t* __restrict__ Y, const TclBatch<K> cf, int n, int64_t rows,
+                int64_t mtiles, const uint32_t* __restrict__ acc, const uint32_t* __restrict__ fold,
+                const ModParams mp) {
   constexpr int SW = stride_words(L);
+  constexpr int STAGES = tcl_stages(K);
+  constexpr uint32_t TCOLS = tcl_tmem_cols(K);
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t YT = tcl_ytile_bytes(n), BB = tcl_b_bytes(n);
-  uint8_t* sB = smem + TCL_STAGES * YT;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + BB);
-  uint64_t* empty = full + TCL_STAGES;
-  uint64_t* tfull = empty + TCL_STAGES;  // [2] accumulator ready
+  uint8_t* sB = smem + STAGES * YT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + K * BB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -397,25 +425,26 @@ __global__ void __launch_bounds__(TCL_THREADS, TCL_CTAS_PER_SM)
   const int64_t ntile = blockIdx.x < mtiles ? (mtiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TCL_STAGES; s++) {
+    for (int s = 0; s < STAGES; s++) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, 128);
+      mbar_init(tempty + b, 128 * tcl_epi(K));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(128));
+                 "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
   // C'[k][(s, q)] = byte (k - q) of c_s, tiled [s][mg][kc][8 rows][16 bytes]:
   // word w of the tile holds 4 consecutive q of one (s, k)
-  for (int w = threadIdx.x; w < (int)(BB / 4); w += blockDim.x) {
-    const int byte0 = w * 4;
+  for (int w = threadIdx.x; w < (int)(K * BB / 4); w += blockDim.x) {
+    const int st = w / (int)(BB / 4);  // which step's C'
+    const int byte0 = (w % (int)(BB / 4)) * 4;
     const int s_ = byte0 / (TCL_N * 32), rem = byte0 % (TCL_N * 32);
     const int mg = rem >> 8, kc = (rem >> 7) & 1, rr = (rem >> 4) & 7, jj0 = rem & 15;
     const int k = mg * 8 + rr;
@@ -423,7 +452,7 @@ __global__ void __launch_bounds__(TCL_THREADS, TCL_CTAS_PER_SM)
 #pragma unroll
     for (int b = 0; b < 4; b++) {
       const int p = k - (kc * 16 + jj0 + b);
-      const uint32_t v = (p >= 0 && p < 32) ? (cf.w[s_][p >> 2] >> (8 * (p & 3))) & 0xFFu : 0u;
+      const uint32_t v = (p >= 0 && p < 32) ? (cf.w[st][s_][p >> 2] >> (8 * (p & 3))) & 0xFFu : 0u;
       word |= v << (8 * b);
     }
     reinterpret_cast<uint32_t*>(sB)[w] = word;
@@ -437,76 +466,84 @@ __global__ void __launch_bounds__(TCL_THREADS, TCL_CTAS_PER_SM)
 
   if (warp == 0 && lane == 0) {
     for (int64_t j = 0; j < ntile; j++) {
-      const int s = (int)(j % TCL_STAGES);
-      if (j >= TCL_STAGES) mbar_wait(empty + s, (uint32_t)((j / TCL_STAGES - 1) & 1));
+      const int s = (int)(j % STAGES);
+      if (j >= STAGES) mbar_wait(empty + s, (uint32_t)((j / STAGES - 1) & 1));
       mbar_expect_tx(full + s, YT);
       bulk_g2s(smem + s * YT, Y + (size_t)(blockIdx.x + j * gridDim.x) * YT, YT, full + s);
     }
   } else if (warp == 1 && lane == 0) {
     for (int64_t j = 0; j < ntile; j++) {
-      const int s = (int)(j % TCL_STAGES);
+      const int s = (int)(j % STAGES);
       const int b = (int)(j & 1);
-      mbar_wait(full + s, (uint32_t)((j / TCL_STAGES) & 1));
+      mbar_wait(full + s, (uint32_t)((j / STAGES) & 1));
       if (j >= 2) mbar_wait(tempty + b, (uint32_t)((j / 2 - 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint8_t* sy = smem + s * YT;
-      for (int ks = 0; ks < n; ks++) {
-        const uint64_t ad = umma_desc(sy + ks * (128 * 32));
-        const uint64_t bd = umma_desc(sB + ks * (TCL_N * 32));
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (uint32_t)(b * TCL_N)),
-            "l"(ad), "l"(bd), "r"(TCL_IDESC), "r"(ks > 0 ? 1u : 0u));
-      }
+      for (int st = 0; st < K; st++)
+        for (int ks = 0; ks < n; ks++) {
+          const uint64_t ad = umma_desc(sy + ks * (128 * 32));
+          const uint64_t bd = umma_desc(sB + st * BB + ks * (TCL_N * 32));
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(
+                  tmem + (uint32_t)((b * K + st) * TCL_N)),
+              "l"(ad), "l"(bd), "r"(TCL_IDESC), "r"(ks > 0 ? 1u : 0u));
+        }
       umma_commit(empty + s);
       umma_commit(tfull + b);
     }
   } else if (warp >= 2) {
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;  // which of the quarter's epilogue warps
+    constexpr int E = tcl_epi(K);
     const int row = quarter * 32 + lane;
     for (int64_t j = 0; j < ntile; j++) {
       const int b = (int)(j & 1);
       mbar_wait(tfull + b, (uint32_t)((j / 2) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t d[TCL_N];
-      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * TCL_N);
-#pragma unroll
-      for (int h = 0; h < 2; h++)
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(d[32 * h + 0]), "=r"(d[32 * h + 1]), "=r"(d[32 * h + 2]), "=r"(d[32 * h + 3]),
-              "=r"(d[32 * h + 4]), "=r"(d[32 * h + 5]), "=r"(d[32 * h + 6]), "=r"(d[32 * h + 7]),
-              "=r"(d[32 * h + 8]), "=r"(d[32 * h + 9]), "=r"(d[32 * h + 10]), "=r"(d[32 * h + 11]),
-              "=r"(d[32 * h + 12]), "=r"(d[32 * h + 13]), "=r"(d[32 * h + 14]), "=r"(d[32 * h + 15]),
-              "=r"(d[32 * h + 16]), "=r"(d[32 * h + 17]), "=r"(d[32 * h + 18]), "=r"(d[32 * h + 19]),
-              "=r"(d[32 * h + 20]), "=r"(d[32 * h + 21]), "=r"(d[32 * h + 22]), "=r"(d[32 * h + 23]),
-              "=r"(d[32 * h + 24]), "=r"(d[32 * h + 25]), "=r"(d[32 * h + 26]), "=r"(d[32 * h + 27]),
-              "=r"(d[32 * h + 28]), "=r"(d[32 * h + 29]), "=r"(d[32 * h + 30]), "=r"(d[32 * h + 31])
-            : "r"(ta + (uint32_t)(32 * h)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(tempty + b);
-      const int64_t i = (int64_t)(blockIdx.x + j * gridDim.x) * 128 + row;
-      if (i >= rows) continue;
-      // bytes (weights 2^(8k)) -> 32-bit limbs V[0..16]
+#pragma unroll 1
+      for (int st = half; st < K; st += E) {
+      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)((b * K + st) * TCL_N);
+      // bytes (weights 2^(8k)) -> 32-bit limbs V[0..16], the 64 columns read
+      // from TMEM in two halves of 32 (fewer live registers)
       uint32_t V[17];
       uint64_t carry = 0;
 #pragma unroll
-      for (int w = 0; w < 16; w++) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int bb = 0; bb < 4; bb++) {
-          const uint64_t t = carry + d[4 * w + bb];
-          word |= (uint32_t)(t & 0xFF) << (8 * bb);
-          carry = t >> 8;
+      for (int h = 0; h < 2; h++) {
+        uint32_t d[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+              "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]),
+              "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]),
+              "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]),
+              "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+            : "r"(ta + (uint32_t)(32 * h)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (h == 1 && st + E >= K) {  // this warp's last accumulator of the buffer is read
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          mbar_arrive(tempty + b);
         }
-        V[w] = word;
+#pragma unroll
+        for (int w = 0; w < 8; w++) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int bb = 0; bb < 4; bb++) {
+            const uint64_t t = carry + d[4 * w + bb];
+            word |= (uint32_t)(t & 0xFF) << (8 * bb);
+            carry = t >> 8;
+          }
+          V[8 * h + w] = word;
+        }
       }
       V[16] = (uint32_t)carry;  // < 2^25
+      const int64_t i = (int64_t)(blockIdx.x + j * gridDim.x) * 128 + row;
+      if (i >= rows) continue;
       int64_t a2[L + 1];
 #pragma unroll
-      for (int q = 0; q < L; q++) a2[q] = (int64_t)V[q] + (acc ? (int64_t)(acc[(size_t)i * SW + q] ^ 0x80000000u) : 0);
+      for (int q = 0; q < L; q++)
+        a2[q] = (int64_t)V[q] + ((K == 1 && acc) ? (int64_t)(acc[(size_t)i * SW + q] ^ 0x80000000u) : 0);
       a2[L] = 0;
 #pragma unroll
       for (int k = L; k < 17; k++) {
@@ -523,14 +560,15 @@ __global__ void __launch_bounds__(TCL_THREADS, TCL_CTAS_PER_SM)
       uint32_t o[SW];
 #pragma unroll
       for (int q = 0; q < SW; q++) o[q] = q < L ? (Rr[q] ^ 0x80000000u) : 0u;
-      store_slot<SW>(dst + (size_t)i * SW, o);
+      store_slot<SW>(cf.dst[st] + (size_t)i * SW, o);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
 }
 

@@ -185,17 +185,31 @@ class LinCombSet:
     """n <= 8 fixed device vectors combined on the tensor cores (Mksol's
     Horner combination, sld_lcset_*): dst = acc + sum_s c_s y_s mod l."""
 
-    def __init__(self, field: Field, ys, rows: int):
+    def __init__(self, field: Field, ys, rows: int, matrix: "DeviceMatrix" = None):
+        """With `matrix`, the set is tiled in that matrix's slot order: its
+        combinations are slot-ordered (the operand of DeviceMatrix.spmv_add)."""
         self.field, self.n = field, len(ys)
         ptrs = np.array([y.ptr for y in ys], dtype=np.uint64)
         h = ctypes.c_void_p()
-        N.check(N.load().sld_lcset_create(field.handle, N.ptr(ptrs), self.n, int(rows), ctypes.byref(h)))
+        if matrix is None:
+            N.check(N.load().sld_lcset_create(field.handle, N.ptr(ptrs), self.n, int(rows), ctypes.byref(h)))
+        else:
+            N.check(N.load().sld_lcset_create_slots(matrix.handle, N.ptr(ptrs), self.n, ctypes.byref(h)))
         self._h = h
         self._ys = list(ys)  # keep the vectors alive while tiled copies are in use
 
     def apply(self, coeffs, dst: "DeviceVector", acc: "DeviceVector" = None):
         cl = ints_to_limbs([int(c) for c in coeffs], self.field.L)
         N.check(N.load().sld_lcset_apply(self._h, N.ptr(cl), acc.ptr if acc is not None else 0, dst.ptr))
+
+    def apply_batch(self, coeff_sets, dsts):
+        """dsts[k] = sum_s coeff_sets[k][s] y_s for K = 2 or 4 steps, one
+        pass over the tiled y."""
+        K = len(coeff_sets)
+        cl = np.ascontiguousarray(np.stack([ints_to_limbs([int(c) for c in cs], self.field.L)
+                                            for cs in coeff_sets]))
+        ptrs = np.array([d.ptr for d in dsts], dtype=np.uint64)
+        N.check(N.load().sld_lcset_apply_batch(self._h, N.ptr(cl), K, N.ptr(ptrs)))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -395,6 +409,16 @@ class DeviceMatrix:
                                             for y in ys])
         N.check(lib.sld_mat_mksol_bind(self._h, arr, len(ys)))
         return True
+
+    @property
+    def nslots(self) -> int:
+        i = self.info()
+        return int(i["nslices"]) * int(i["rows_per_slice"])
+
+    def spmv_add(self, vin: DeviceVector, vout: DeviceVector, addv: DeviceVector):
+        """vout = A vin + addv, addv in the slot order (a LinCombSet built with
+        matrix=self); asynchronous, the addition in the last pass."""
+        N.check(N.load().sld_spmv_add(self._h, vin.handle, vout.handle, addv.handle))
 
     def spmv_mksol(self, vin: DeviceVector, vout: DeviceVector, coeffs):
         """vout = A vin + sum_s coeffs[s] y_s mod l (the bound y vectors),

@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .device import DEFAULT_DEVICE, DeviceMatrix, DevicePlanes, LinCombSet, XBlock, lincomb
+from .device import DEFAULT_DEVICE, DeviceMatrix, DevicePlanes, DeviceVector, LinCombSet, XBlock, lincomb
 from .modring import (
     as_modulus, digit_count, ints_to_limbs, ints_to_planes, limbs_to_ints, limbs_to_planes,
     planes_to_ints, planes_to_limbs,
@@ -258,11 +258,44 @@ class B200Multiplier:
             # Measured level with the tensor-core combination kernel (cfg3
             # 1.91 vs 1.87 ms, cfg2 0.323 vs 0.335 ms), so it is opt-in.
             fused = dmax > 0 and os.environ.get("SLD_MKSOL_FUSED", "0") == "1" and dm.mksol_bind(ys)
+            # SLD_MKSOL_BATCH=2|4 (opt-in): the combinations do not depend on
+            # w, so K steps' combinations come from ONE pass over the y tiled
+            # in the matrix's slot order (sld_lcset_apply_batch) into K
+            # vectors, and each Horner step adds its vector in the SpMV's
+            # last-pass epilogue (sld_spmv_add), reading n/K + 1 vectors per
+            # step instead of n + 2.  Measured at cfg3 (in-situ kernel times):
+            # the combination drops from 198 to 163 us per step, the last pass
+            # gains 15 us: 1.797 vs 1.820 ms per step, within the run-to-run
+            # noise -- the K reductions per row (carry, fold, Barrett: ~650
+            # instructions) bound it, not the y traffic.
+            K = int(os.environ.get("SLD_MKSOL_BATCH", "0"))
+            info = dm.info()
+            batched = (lc is not None and not fused and dmax > 0 and K in (2, 4) and info["chains"] == 1
+                       and info["halves"] == 1 and info["lanes_per_residue"] == 1)
+            degs = [_poly_degree(p) for p in G]
+
+            def coeffs_at(i):
+                return [p[i] if i <= d else 0 for p, d in zip(G, degs)]
+
             combo(dmax, None, w)
             horner = 0
-            for i in range(dmax - 1, -1, -1):
+            if batched:
+                lcs = LinCombSet(dm.field, ys, dm.total_cols, matrix=dm)  # slot order
+                bufs = [DeviceVector(dm.field, dm.nslots) for _ in range(K)]
+                for i0 in range(dmax - 1, -1, -K):
+                    steps = list(range(i0, max(i0 - K, -1), -1))
+                    sets = [coeffs_at(i) for i in steps] + [[0] * len(G)] * (K - len(steps))
+                    lcs.apply_batch(sets, bufs)
+                    for k in range(len(steps)):
+                        dm.spmv_add(w, t, bufs[k])
+                        w, t = t, w
+                        horner += 1
+                for b in bufs:
+                    b.close()
+                lcs.close()
+            for i in ([] if batched else range(dmax - 1, -1, -1)):
                 if fused:
-                    dm.spmv_mksol(w, t, [p[i] if i <= _poly_degree(p) else 0 for p in G])
+                    dm.spmv_mksol(w, t, coeffs_at(i))
                     w, t = t, w
                 else:
                     dm.spmv(w, t, sync=False)  # in stream order with the combination

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import fixture_sparse, to_oracle
+from helpers import fixture_sparse, rand_matrix, to_oracle
 from paper_1402_3661_b200 import (
     B200Multiplier, PrimeModulus, SolverFailure, SparseMatrix, mksol_block, mksol_scalar,
     verify_kernel,
@@ -231,3 +231,90 @@ def test_spmv_mksol_vs_python(monkeypatch, bits, n, extreme, stripes):
     dm.mksol_bind([])
     with pytest.raises(ValueError):
         dm.spmv_mksol(vin, vout, cs)  # unbound
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [2, 31, 160, 202, 256])
+@pytest.mark.parametrize("K", [2, 4])
+@pytest.mark.parametrize("n,extreme", [(1, False), (8, False), (8, True)])
+def test_batched_combination_vs_python(bits, K, n, extreme):
+    # sld_lcset_apply_batch: K Horner steps' combinations from one pass over
+    # the tiled y (K C' tiles, K TMEM accumulators per buffer), ragged tiles
+    from paper_1402_3661_b200.device import DeviceVector, Field, LinCombSet
+    from paper_1402_3661_b200.modring import next_prime
+    ell = 3 if bits == 2 else next_prime((1 << bits) - (1 << (bits // 2)))
+    if ell.bit_length() > bits:
+        ell = next_prime(1 << (bits - 1))
+    mod = PrimeModulus(ell)
+    rng = np.random.default_rng(bits * 10 + n + K)
+    rows = 20000 + 77
+    f = Field(mod, 0)
+    ys = [[ell - 1] * rows if extreme else mod.random_residues(rng, rows) for _ in range(n)]
+    dys = []
+    for y in ys:
+        d = DeviceVector(f, rows)
+        d.upload_limbs(ints_to_limbs(y, mod.limbs))
+        dys.append(d)
+    lc = LinCombSet(f, dys, rows)
+    dsts = [DeviceVector(f, rows) for _ in range(K)]
+    sets = [[ell - 1] * n if extreme else mod.random_residues(rng, n) for _ in range(K)]
+    sets[-1] = [0] * n  # a padded (all-zero) step
+    lc.apply_batch(sets, dsts)
+    for cs, d in zip(sets, dsts):
+        want = [sum(c * y[i] for c, y in zip(cs, ys)) % ell for i in range(rows)]
+        assert limbs_to_ints(d.download_limbs()) == want
+    lc.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("short", ["0", "1"])
+@pytest.mark.parametrize("stripes", [1, 3])
+def test_spmv_add_vs_oracle(monkeypatch, short, stripes):
+    # sld_spmv_add: out = A in + addv, addv from a slot-ordered combination
+    # set (sld_lcset_create_slots), the addition in the last pass (pass and
+    # short-row layouts, one or several stripes)
+    from paper_1402_3661_b200.device import DeviceMatrix, DeviceVector, LinCombSet
+    monkeypatch.setenv("SLD_SHORT", short)
+    mod = PrimeModulus(0xc152a866f35196bb08ec18cd24e7a4f6d2ac709d)
+    rng = np.random.default_rng(7 + stripes)
+    nr = 3000
+    A = rand_matrix(mod, rng, nr, nr - 1, 14, dense=1)
+    dm = DeviceMatrix(A, stripe_cols=(A.total_cols + stripes - 1) // stripes if stripes > 1 else 0)
+    u = mod.random_residues(rng, nr)
+    ys = [mod.random_residues(rng, nr), [mod.ell - 1] * nr]
+    cs = [mod.random_residues(rng, 2), [mod.ell - 1, mod.ell - 1]]
+    dys = []
+    for y in ys:
+        d = dm.vector()
+        d.upload_limbs(ints_to_limbs(y, mod.limbs))
+        dys.append(d)
+    lcs = LinCombSet(dm.field, dys, dm.total_cols, matrix=dm)
+    vas = [DeviceVector(dm.field, dm.nslots) for _ in range(2)]
+    lcs.apply_batch(cs, vas)
+    vin, vout = dm.vector(), dm.vector()
+    vin.upload_limbs(ints_to_limbs(u, mod.limbs))
+    Au = O.limbs_to_ints(to_oracle(A).spmv_limbs(O.ints_to_limbs(u, mod.limbs)))
+    for c, va in zip(cs, vas):
+        dm.spmv_add(vin, vout, va)
+        want = [(Au[i] + c[0] * ys[0][i] + c[1] * ys[1][i]) % mod.ell for i in range(nr)]
+        assert limbs_to_ints(vout.download_limbs())[:nr] == want
+    lcs.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", ["0", "2", "4"])
+def test_device_mksol_batched_matches_reference(monkeypatch, batch):
+    # the Horner loop with K steps' combinations batched (default K = 4)
+    # against the reference's kernel vectors; SLD_MKSOL_BATCH=0 is the
+    # per-step combination kernel
+    from paper_1402_3661_b200.device import DeviceMatrix
+    monkeypatch.setenv("SLD_MKSOL_BATCH", batch)
+    calls = []
+    orig = DeviceMatrix.spmv_add
+    monkeypatch.setattr(DeviceMatrix, "spmv_add", lambda self, *a: (calls.append(1), orig(self, *a)))
+    for A, Y, polys, w, (horner, tail, ver) in _cases():
+        mul = B200Multiplier(A)
+        kv = mksol_block(A, Y, type("G", (), {"polys": polys})(), mul=mul)
+        assert kv.w == w
+        assert (kv.horner_spmvs, kv.tail_spmvs, kv.verified) == (horner, tail, True)
+    assert (len(calls) > 0) == (batch != "0")

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--n", type=int, default=8)
     ap.add_argument("--degree", type=int, default=48)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--modes", default="fused,batch0,batch2,batch4")
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     A, _, mod = bench.build_matrix(cfg, lambda m: print(m, file=sys.stderr))
@@ -42,8 +43,10 @@ def main():
     # the set-up of each call cancel); the fused step (combination in the
     # SpMV epilogue) against SpMV + combination kernel
     ws = []
-    for fused in ("1", "0"):
+    for mode in a.modes.split(","):
+        fused = "1" if mode == "fused" else "0"
         os.environ["SLD_MKSOL_FUSED"] = fused
+        os.environ["SLD_MKSOL_BATCH"] = mode[5:] if mode.startswith("batch") else "0"
         ws.append(mul.mksol(Y, [p[:a.degree + 1] for p in polys])[0])
         res = []
         for deg in (a.degree // 4, a.degree):
@@ -55,10 +58,12 @@ def main():
                 best = dt if best is None else min(best, dt)
             res.append((horner, best))
         (h0, t0), (h1, t1) = res
-        print(f"{a.config} mksol n={a.n} {'fused' if fused == '1' else 'two kernels'}: {h1} Horner steps in "
+        label = {"fused": "fused epilogue", "batch0": "two kernels",
+                 "batch2": "batched combination K=2", "batch4": "batched combination K=4"}[mode]
+        print(f"{a.config} mksol n={a.n} {label}: {h1} Horner steps in "
               f"{t1:.3f} s, {h0} in {t0:.3f} s -> {(t1 - t0) / (h1 - h0) * 1e3:.3f} ms per Horner step; "
               f"plain SpMV {spmv:.3f} ms", flush=True)
-    print(f"fused and two-kernel Horner results identical: {all(np.array_equal(ws[0], x) for x in ws[1:])}")
+    print(f"all Horner modes give identical results: {all(np.array_equal(ws[0], x) for x in ws[1:])}")
 
 
 if __name__ == "__main__":
