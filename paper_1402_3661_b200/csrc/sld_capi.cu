@@ -1292,6 +1292,12 @@ extern "C" int sld_mat_create_chains(sld_ctx* ctx, int chains, int64_t nrows, in
     int sh = (chains == 1 && ctx->SW <= 8 && nrows < 32LL * 16 * ctx->sms) ? 1 : 0;
     if (const char* pe = getenv("SLD_SHORT")) sh = atoi(pe) && chains == 1 && ctx->SW <= 8;
     M->short_rows = sh;
+    // index prefetch two groups ahead, except for the one-chain pass layout,
+    // whose one-sector gathers already saturate the SM's request interface:
+    // there the prefetches are requests that cost more than they hide (cfg3
+    // 1.581 vs 1.607 ms, cfg2 0.2747 vs 0.2762 ms; the limb-sliced cfg5
+    // wants them: 0.997 vs 1.055 ms; profiles/sweep_pf_g1_r02.txt)
+    if (!getenv("SLD_PF")) M->pf = (chains == 1 && !M->sliced && !M->short_rows) ? 0 : 2;
   }
   if (const char* pe = getenv("SLD_CHAIN")) M->chain_ok = atoi(pe) != 0;
   if (const char* pe = getenv("SLD_APW")) M->apw = atoi(pe);

@@ -124,7 +124,7 @@ struct sld_mat {
   int64_t max_deg = 0;
   size_t dev_bytes = 0;
   int policy = 7;  // L2 policy bits (SpmvArgs::policy), measured best; env SLD_POLICY overrides
-  int pf = 2;      // index prefetch distance in groups, measured; env SLD_PF overrides
+  int pf = 2;      // index prefetch distance in groups (0 for one-chain passes), measured; env SLD_PF overrides
   int apw = 0;       // persisting L2 access-policy window over the gathered stripe (env SLD_APW)
   float apw_ratio = 1.0f;
   // device
