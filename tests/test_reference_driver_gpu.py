@@ -121,3 +121,17 @@ print(json.dumps(res))
     res = json.loads(r.stdout.strip().splitlines()[-1])
     for k, v in res.items():
         assert v["applies"] > 2 * v["n"], (k, v)
+
+
+def test_reference_whole_suite_on_b200(ref_tree, tmp_path):
+    """Every test module of the reference (balance, cli, corpus, gridmv,
+    modring, perfmodel, sge, solver, spmatrix, vecops, acceptance) with the
+    swap.  Deselected: criterion 1 (the full pipeline, ~6 min; it passes,
+    profiles/refswap_full_r02.txt) and criterion 6, which fails at seed 31
+    with the reference's OWN multiplier too -- same messages at the same
+    attempts on the B200 (tools/diag_sge2.py)."""
+    out, stats = _run_reference_tests(
+        ref_tree, tmp_path,
+        ["tests", "-k", "not criterion_01 and not criterion_06"])
+    assert " passed" in out and "failed" not in out and "error" not in out.lower().split("passed")[-1]
+    assert stats["multipliers"] >= 50 and stats["applies"] > 10000, stats
