@@ -16,7 +16,7 @@ OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libsldb200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                      "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
 if os.environ.get("SLD_NVCC_EXTRA"):
     NVCC_FLAGS += os.environ["SLD_NVCC_EXTRA"].split()

@@ -527,6 +527,94 @@ static void host_par(int64_t n, F f) {
 
 static constexpr int64_t XFER_CHUNK = 1 << 19;  // rows per DMA chunk
 
+// digit planes (P 16-bit digits per residue, one per uint64 cell: the
+// reference's format, vecops.py:22-47) <-> L 32-bit limbs, n residues.  The
+// repack runs at host memory speed only when the limb count is a compile-time
+// constant (unrolled, vectorisable): one instance per L, P = 2L or 2L - 1
+// (the widths a modulus of L limbs has), a generic loop otherwise.
+template <int L>
+static void pack_planes(const uint64_t* __restrict__ src, int P, uint32_t* __restrict__ dst, int64_t n) {
+  if (P == 2 * L) {
+    for (int64_t r = 0; r < n; r++) {
+      const uint64_t* s = src + r * (2 * L);
+      uint32_t* d = dst + r * L;
+#pragma GCC unroll 32
+      for (int j = 0; j < L; j++) d[j] = (uint32_t)(s[2 * j] & 0xFFFF) | ((uint32_t)(s[2 * j + 1] & 0xFFFF) << 16);
+    }
+  } else if (P == 2 * L - 1) {
+    for (int64_t r = 0; r < n; r++) {
+      const uint64_t* s = src + r * (2 * L - 1);
+      uint32_t* d = dst + r * L;
+#pragma GCC unroll 32
+      for (int j = 0; j < L - 1; j++)
+        d[j] = (uint32_t)(s[2 * j] & 0xFFFF) | ((uint32_t)(s[2 * j + 1] & 0xFFFF) << 16);
+      d[L - 1] = (uint32_t)(s[2 * L - 2] & 0xFFFF);
+    }
+  } else {
+    for (int64_t r = 0; r < n; r++) {
+      const uint64_t* s = src + r * P;
+      for (int j = 0; j < L; j++) {
+        const uint32_t d0 = 2 * j < P ? (uint32_t)(s[2 * j] & 0xFFFF) : 0u;
+        const uint32_t d1 = 2 * j + 1 < P ? (uint32_t)(s[2 * j + 1] & 0xFFFF) : 0u;
+        dst[r * L + j] = d0 | (d1 << 16);
+      }
+    }
+  }
+}
+
+template <int L>
+static void unpack_planes(const uint32_t* __restrict__ src, uint64_t* __restrict__ dst, int P, int64_t n) {
+  if (P == 2 * L) {
+    for (int64_t r = 0; r < n; r++) {
+      const uint32_t* s = src + r * L;
+      uint64_t* d = dst + r * (2 * L);
+#pragma GCC unroll 32
+      for (int j = 0; j < L; j++) {
+        d[2 * j] = s[j] & 0xFFFF;
+        d[2 * j + 1] = s[j] >> 16;
+      }
+    }
+  } else if (P == 2 * L - 1) {
+    for (int64_t r = 0; r < n; r++) {
+      const uint32_t* s = src + r * L;
+      uint64_t* d = dst + r * (2 * L - 1);
+#pragma GCC unroll 32
+      for (int j = 0; j < L - 1; j++) {
+        d[2 * j] = s[j] & 0xFFFF;
+        d[2 * j + 1] = s[j] >> 16;
+      }
+      d[2 * L - 2] = s[L - 1] & 0xFFFF;
+    }
+  } else {
+    for (int64_t r = 0; r < n; r++)
+      for (int q = 0; q < P; q++) {
+        const int j = q >> 1;
+        const uint32_t w = j < L ? src[r * L + j] : 0u;
+        dst[r * P + q] = (q & 1) ? (w >> 16) : (w & 0xFFFF);
+      }
+  }
+}
+
+using PackFn = void (*)(const uint64_t*, int, uint32_t*, int64_t);
+using UnpackFn = void (*)(const uint32_t*, uint64_t*, int, int64_t);
+template <int L>
+static void fill_pack(PackFn* p, UnpackFn* u) {
+  p[L] = pack_planes<L>;
+  u[L] = unpack_planes<L>;
+  if constexpr (L > 1) fill_pack<L - 1>(p, u);
+}
+static const PackFn* pack_tab(UnpackFn** u_out) {
+  static PackFn p[MAXL + 1];
+  static UnpackFn u[MAXL + 1];
+  static bool init = [] {
+    fill_pack<MAXL>(p, u);
+    return true;
+  }();
+  (void)init;
+  *u_out = u;
+  return p;
+}
+
 // rows of planes (P 16-bit digits in uint64 cells) or limbs (L words) -> device slots
 // planes of chain g at planes_g[g] (nullptr: all chains contiguous at `planes`)
 static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs, int64_t rows, int P,
@@ -539,18 +627,20 @@ static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs
   TRY(ensure_stage(c, bytes));
   uint32_t* h = (uint32_t*)c->hstage;
   uint32_t* d = (uint32_t*)c->dstage;
+  UnpackFn* ut;
+  const PackFn pack = pack_tab(&ut)[L];
   for (int64_t lo = 0; lo < n; lo += XFER_CHUNK) {
     const int64_t hi = std::min(n, lo + XFER_CHUNK);
     host_par(hi - lo, [&](int64_t a, int64_t b) {
+      if (planes && !planes_g) {  // one contiguous run of rows
+        pack(planes + (size_t)(lo + a) * P, P, h + (size_t)(lo + a) * L, b - a);
+        return;
+      }
       for (int64_t r = lo + a; r < lo + b; r++) {
         uint32_t* dst = h + (size_t)r * L;
         if (planes || planes_g) {
           const uint64_t* src = planes_g ? planes_g[r / rows] + (size_t)(r % rows) * P : planes + (size_t)r * P;
-          for (int j = 0; j < L; j++) {
-            const uint32_t d0 = 2 * j < P ? (uint32_t)(src[2 * j] & 0xFFFF) : 0u;
-            const uint32_t d1 = 2 * j + 1 < P ? (uint32_t)(src[2 * j + 1] & 0xFFFF) : 0u;
-            dst[j] = d0 | (d1 << 16);
-          }
+          pack(src, P, dst, 1);
         } else {
           memcpy(dst, limbs + (size_t)r * L, 4 * (size_t)L);
         }
@@ -575,6 +665,9 @@ static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t 
   TRY(ensure_stage(c, bytes));
   uint32_t* h = (uint32_t*)c->hstage;
   uint32_t* d = (uint32_t*)c->dstage;
+  UnpackFn* ut;
+  pack_tab(&ut);
+  const UnpackFn unpack = ut[L];
   ops(L).slots_to_limbs(v->buf[v->cur], n, d, 0x80000000u, rows, v->chains, c->stream);
   CU(cudaGetLastError());
   std::vector<cudaEvent_t> ev;
@@ -595,15 +688,15 @@ static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t 
     if (e != cudaSuccess && rc == SLD_OK) rc = fail(SLD_E_CUDA, "download: %s", cudaGetErrorString(e));
     if (rc != SLD_OK) continue;
     host_par(hi - lo, [&](int64_t a, int64_t b) {
+      if (planes && !planes_g) {
+        unpack(h + (size_t)(lo + a) * L, planes + (size_t)(lo + a) * P, P, b - a);
+        return;
+      }
       for (int64_t r = lo + a; r < lo + b; r++) {
         const uint32_t* src = h + (size_t)r * L;
         if (planes || planes_g) {
           uint64_t* dst = planes_g ? planes_g[r / rows] + (size_t)(r % rows) * P : planes + (size_t)r * P;
-          for (int q = 0; q < P; q++) {
-            const int j = q >> 1;
-            const uint32_t w = j < L ? src[j] : 0u;
-            dst[q] = (q & 1) ? (w >> 16) : (w & 0xFFFF);
-          }
+          unpack(src, dst, P, 1);
         } else {
           memcpy(limbs + (size_t)r * L, src, 4 * (size_t)L);
         }

@@ -365,6 +365,11 @@ class DeviceMatrix:
     # a few spare iterate buffers, recycled by DevicePlanes (one chain)
     _POOL_MAX = 4
 
+    def copy_vector(self, src: DeviceVector, dst: DeviceVector):
+        """dst = src on the device (one add_mod of a single term)."""
+        ptrs = np.array([src.ptr], dtype=np.uint64)
+        N.check(N.load().sld_add_mod(self.field.handle, N.ptr(ptrs), 1, dst.ptr, src.n))
+
     def pool_get(self):
         pool = self.__dict__.setdefault("_pool", [])
         return pool.pop() if pool else self.vector()

@@ -195,27 +195,34 @@ class B200Multiplier:
 
     def krylov(self, xblock, v_planes, steps):
         """`steps` chain steps on the device from iterate `v_planes`:
-        returns (terms as list of m-int lists, final iterate planes)."""
+        returns (terms as list of m-int lists, final iterate).  The final
+        iterate stays on the device as `DevicePlanes`, like `.apply`'s result:
+        the planes array on any host access (one download then), and passed
+        back in (the next checkpoint chunk) it is copied on the device, not
+        uploaded."""
         with self._lock:
             dm = self.dm
-            P = v_planes.shape[1]
-            if getattr(self, "_vec", None) is None:
-                self._vec = dm.vector()  # kept: device iterate + its ping-pong twin
-            vec = self._vec
-            vec.upload_planes(v_planes)
+            vec = dm.pool_get()  # device iterate + its ping-pong twin, recycled
+            if isinstance(v_planes, DevicePlanes) and v_planes._dm is dm:
+                P = v_planes._P
+                dm.copy_vector(v_planes._vec, vec)  # the input object stays untouched
+            else:
+                p = np.ascontiguousarray(v_planes, dtype=np.uint64)
+                P = p.shape[1]
+                vec.upload_planes(p)
             if isinstance(xblock, UnitRows):
                 terms = dm.krylov_unit(vec, xblock.rows, steps)
             elif isinstance(xblock, DenseRows) or hasattr(xblock, "vectors"):
                 db = xblock if isinstance(xblock, DenseRows) else DenseRows(xblock.vectors, self.mod)
                 terms = dm.krylov_dense(vec, db.device_block(dm), steps)
             else:
+                dm.pool_put(vec)
                 raise TypeError(f"unsupported projection block {type(xblock).__name__}")
-            v_out = vec.download_planes(P)
         self.count += int(steps)
         m = terms.shape[1]
         flat = limbs_to_ints(terms.reshape(-1, terms.shape[2])) if terms.size else []
         out = [flat[i * m:(i + 1) * m] for i in range(int(steps))]
-        return out, v_out
+        return out, DevicePlanes(dm, vec, P)
 
 
     def mksol(self, Y_planes, polys):
