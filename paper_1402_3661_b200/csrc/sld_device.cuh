@@ -1037,11 +1037,39 @@ __global__ void __launch_bounds__(256, SLD_WIDE_MINB) spmv_wide(const SpmvArgs a
     for (int k = SW - 1; k >= L; k--) hi = (hi << 32) + W[k];
     acc2[L] = (int64_t)hi;
   }
+  // Lazy partials between the passes (SW >= L + 2): a pass that is not the
+  // last stores its row value V exactly -- words 0..L-1 and the signed int64
+  // of the words above -- instead of reducing it; the next pass adds it to
+  // its sums and only the last pass runs Barrett.  |V| < 2^47 ell per pass
+  // (the row bounds of mat_build), so the words above L stay below 2^48 in
+  // total over the passes.  Saves one L-limb Barrett per row and pass, run by
+  // one lane of T (cfg5: ~0.1 ms per extra pass).
+  constexpr bool LAZY = SW >= L + 2;
   if (!FIRST) {
     uint32_t pin[SW];
     load_slot<SW>(a.part_in + (size_t)slot * SW, pin, pol);
 #pragma unroll
     for (int i = 0; i < L; i++) acc2[i] += pin[i];
+    if constexpr (LAZY) acc2[L] += (int64_t)((uint64_t)pin[L] | ((uint64_t)pin[L + 1] << 32));
+  }
+  if constexpr (LAZY && !LAST) {
+    uint32_t o[SW];
+    int64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < L; i++) {
+      const int64_t t = acc2[i] + c;
+      o[i] = (uint32_t)t;
+      c = t >> 32;
+    }
+    const int64_t hi = acc2[L] + c;
+    o[L] = (uint32_t)hi;
+    o[L + 1] = (uint32_t)((uint64_t)hi >> 32);
+#pragma unroll
+    for (int i = L + 2; i < SW; i++) o[i] = 0u;
+    uint32_t* dst = a.part_out + (size_t)slot * SW;
+    if (a.policy & 4) store_slot_hint<SW>(dst, o, pol);
+    else store_slot<SW>(dst, o);
+    return;
   }
   // (full-class entries and dense columns: full_fixup after the last pass --
   // their Montgomery products inline made every row of the last pass spill)
