@@ -357,7 +357,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 
 // the +-1 and small entries of one row in one part (column stripe [x half]);
 // with K lanes per row (short rows) lane `sub` takes groups sub, sub+K, ...
-template <int L, int G, int K = 1, bool COH = false>
+template <int L, int G, int K = 1, bool COH = false, bool PIPE = true>
 __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& si, uint32_t kk, int rw,
                                             const uint32_t* xc, uint64_t pol, uint64_t gpol,
                                             int64_t (&acc)[L + 1], int64_t& S, int sub = 0) {
@@ -369,10 +369,19 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
   const uint4* pp = a.pm_idx + si.pm_off + rw;
 #pragma unroll 1
   for (uint32_t k = sub; k < PF && k < my_pm; k += K) prefetch_l2(pp + (size_t)k * R);
+  // PIPE: the next group's index words are loaded before this group's
+  // gathers issue (one register quad of software pipelining), so the index
+  // latency hides behind the gathers without the extra requests of L2
+  // prefetches.  Measured on one box (A/B builds): cfg3 G=1 1.575 -> 1.559
+  // ms, G=2 1.354 -> 1.289 ms per chain-product (profiles/sweep_idx_pipe_r02.txt); the single-pass one-chain
+  // kernel (cfg2) is 1% slower with it and keeps the plain loop.
+  uint4 w_next = make_uint4(0u, 0u, 0u, 0u);
+  if (PIPE && sub < my_pm) w_next = ld_stream(pp + (size_t)sub * R, pol);
 #pragma unroll 1
   for (uint32_t k = sub; k < my_pm; k += K) {
     if (PF && k + PF < my_pm) prefetch_l2(pp + (size_t)(k + PF) * R);
-    const uint4 w = ld_stream(pp + (size_t)k * R, pol);
+    const uint4 w = PIPE ? w_next : ld_stream(pp + (size_t)k * R, pol);
+    if (PIPE && k + K < my_pm) w_next = ld_stream(pp + (size_t)(k + K) * R, pol);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
     for (int e0 = 0; e0 < 4; e0 += NB) {
@@ -606,7 +615,7 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
 #pragma unroll
   for (int i = 0; i <= L; i++) acc[i] = 0;
   int64_t S = 0;  // sum of coefficients (bias correction)
-  row_entries<L, G>(a, si, kk, rw, xc, pol, gpol, acc, S);
+  row_entries<L, G, 1, false, !(FIRST && LAST && G == 1)>(a, si, kk, rw, xc, pol, gpol, acc, S);
   if (!FIRST) {
     uint32_t pin[SW];
     load_slot<SW>(a.part_in + ((size_t)slot * G + chain) * SW, pin, pol);
@@ -665,7 +674,7 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const Sp
 #pragma unroll
   for (int i = 0; i <= L; i++) acc[i] = 0;
   int64_t S = 0;
-  row_entries<L, 1, SHORT_K>(a, si, kk, rw, a.x, pol, gpol, acc, S, sub);
+  row_entries<L, 1, SHORT_K, false, false>(a, si, kk, rw, a.x, pol, gpol, acc, S, sub);
   // the partial and the full-class entries go into other lanes' sums before
   // the reduction, so their loads overlap instead of trailing the row's tail
   if (!FIRST && sub == 2) {
