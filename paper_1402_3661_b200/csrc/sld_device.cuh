@@ -357,7 +357,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 
 // the +-1 and small entries of one row in one part (column stripe [x half]);
 // with K lanes per row (short rows) lane `sub` takes groups sub, sub+K, ...
-template <int L, int G, int K = 1, bool COH = false, bool PIPE = true>
+template <int L, int G, int K = 1, bool COH = false, int PIPE = 1, bool SPIPE = false>
 __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& si, uint32_t kk, int rw,
                                             const uint32_t* xc, uint64_t pol, uint64_t gpol,
                                             int64_t (&acc)[L + 1], int64_t& S, int sub = 0) {
@@ -369,19 +369,37 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
   const uint4* pp = a.pm_idx + si.pm_off + rw;
 #pragma unroll 1
   for (uint32_t k = sub; k < PF && k < my_pm; k += K) prefetch_l2(pp + (size_t)k * R);
-  // PIPE: the next group's index words are loaded before this group's
-  // gathers issue (one register quad of software pipelining), so the index
-  // latency hides behind the gathers without the extra requests of L2
-  // prefetches.  Measured on one box (A/B builds): cfg3 G=1 1.575 -> 1.559
-  // ms, G=2 1.354 -> 1.289 ms per chain-product (profiles/sweep_idx_pipe_r02.txt); the single-pass one-chain
-  // kernel (cfg2) is 1% slower with it and keeps the plain loop.
-  uint4 w_next = make_uint4(0u, 0u, 0u, 0u);
-  if (PIPE && sub < my_pm) w_next = ld_stream(pp + (size_t)sub * R, pol);
+  // PIPE (1 or 2): the index words of the next one or two groups are loaded
+  // before this group's gathers issue (register quads of software
+  // pipelining), so the index latency hides behind the gathers without the
+  // extra requests of L2 prefetches; SPIPE does the same for the small
+  // entries' index and coefficient words.  Measured with A/B builds on one
+  // box (profiles/sweep_idx_pipe_r02.txt): cfg3 one chain 1.575 (none) ->
+  // 1.559 (PIPE 1) -> 1.535-1.542 ms (PIPE 2 + SPIPE); two chains 1.354 ->
+  // 1.289-1.296 ms per chain-product with PIPE 1 and worse with more; the
+  // single-pass one-chain kernel (cfg2) is 1% slower with any and keeps the
+  // plain loop.
+  constexpr bool SP = PIPE > 0 && SPIPE;
+  uint4 w_next = make_uint4(0u, 0u, 0u, 0u), w_next2 = make_uint4(0u, 0u, 0u, 0u);
+  if (PIPE > 0 && sub < my_pm) w_next = ld_stream(pp + (size_t)sub * R, pol);
+  if (PIPE > 1 && sub + K < my_pm) w_next2 = ld_stream(pp + (size_t)(sub + K) * R, pol);
+  const uint4* sp = a.s_idx + si.s_off + rw;
+  const int4* cp = a.s_coef + si.s_off + rw;
+  // with K lanes per row, small group 0 goes to the lane after the one that
+  // took the last +-1 group, so the row's groups spread evenly over its lanes
+  const uint32_t s0 = K > 1 ? (uint32_t)(sub + K - (int)(my_pm % K)) % K : 0u;
+  uint4 sw_next = make_uint4(0u, 0u, 0u, 0u);
+  int4 sc_next = make_int4(0, 0, 0, 0);
 #pragma unroll 1
   for (uint32_t k = sub; k < my_pm; k += K) {
     if (PF && k + PF < my_pm) prefetch_l2(pp + (size_t)(k + PF) * R);
-    const uint4 w = PIPE ? w_next : ld_stream(pp + (size_t)k * R, pol);
-    if (PIPE && k + K < my_pm) w_next = ld_stream(pp + (size_t)(k + K) * R, pol);
+    const uint4 w = PIPE > 0 ? w_next : ld_stream(pp + (size_t)k * R, pol);
+    if (PIPE > 1) {
+      w_next = w_next2;
+      if (k + 2 * K < my_pm) w_next2 = ld_stream(pp + (size_t)(k + 2 * K) * R, pol);
+    } else if (PIPE > 0 && k + K < my_pm) {
+      w_next = ld_stream(pp + (size_t)(k + K) * R, pol);
+    }
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
     for (int e0 = 0; e0 < 4; e0 += NB) {
@@ -400,11 +418,10 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
   }
   // small entries: one signed IMAD.WIDE per limb, the 64-bit product split
   // into its low word (limb i) and signed high word (limb i+1)
-  const uint4* sp = a.s_idx + si.s_off + rw;
-  const int4* cp = a.s_coef + si.s_off + rw;
-  // with K lanes per row, small group 0 goes to the lane after the one that
-  // took the last +-1 group, so the row's groups spread evenly over its lanes
-  const uint32_t s0 = K > 1 ? (uint32_t)(sub + K - (int)(my_pm % K)) % K : 0u;
+  if (SP && s0 < my_s) {
+    sw_next = ld_stream(sp + (size_t)s0 * R, pol);
+    sc_next = ld_stream(cp + (size_t)s0 * R, pol);
+  }
 #pragma unroll 1
   for (uint32_t k = s0; k < PF && k < my_s; k += K) {
     prefetch_l2(sp + (size_t)k * R);
@@ -416,8 +433,12 @@ __device__ __forceinline__ void row_entries(const SpmvArgs& a, const SliceInfo& 
       prefetch_l2(sp + (size_t)(k + PF) * R);
       prefetch_l2(cp + (size_t)(k + PF) * R);
     }
-    const uint4 w = ld_stream(sp + (size_t)k * R, pol);
-    const int4 cf = ld_stream(cp + (size_t)k * R, pol);
+    const uint4 w = SP ? sw_next : ld_stream(sp + (size_t)k * R, pol);
+    const int4 cf = SP ? sc_next : ld_stream(cp + (size_t)k * R, pol);
+    if (SP && k + K < my_s) {
+      sw_next = ld_stream(sp + (size_t)(k + K) * R, pol);
+      sc_next = ld_stream(cp + (size_t)(k + K) * R, pol);
+    }
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
     const int32_t cs[4] = {cf.x, cf.y, cf.z, cf.w};
 #pragma unroll
@@ -615,7 +636,9 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_pass(const Spm
 #pragma unroll
   for (int i = 0; i <= L; i++) acc[i] = 0;
   int64_t S = 0;  // sum of coefficients (bias correction)
-  row_entries<L, G, 1, false, !(FIRST && LAST && G == 1)>(a, si, kk, rw, xc, pol, gpol, acc, S);
+  constexpr bool ONE_PASS_ONE_CHAIN = FIRST && LAST && G == 1;
+  row_entries<L, G, 1, false, ONE_PASS_ONE_CHAIN ? 0 : (G == 1 ? 2 : 1), G == 1 && !ONE_PASS_ONE_CHAIN>(
+      a, si, kk, rw, xc, pol, gpol, acc, S);
   if (!FIRST) {
     uint32_t pin[SW];
     load_slot<SW>(a.part_in + ((size_t)slot * G + chain) * SW, pin, pol);
@@ -674,7 +697,7 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const Sp
 #pragma unroll
   for (int i = 0; i <= L; i++) acc[i] = 0;
   int64_t S = 0;
-  row_entries<L, 1, SHORT_K, false, false>(a, si, kk, rw, a.x, pol, gpol, acc, S, sub);
+  row_entries<L, 1, SHORT_K, false, 0>(a, si, kk, rw, a.x, pol, gpol, acc, S, sub);
   // the partial and the full-class entries go into other lanes' sums before
   // the reduction, so their loads overlap instead of trailing the row's tail
   if (!FIRST && sub == 2) {
