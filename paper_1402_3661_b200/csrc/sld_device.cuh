@@ -970,6 +970,17 @@ __global__ void __launch_bounds__(256, SLD_WIDE_MINB) spmv_wide(const SpmvArgs a
   int64_t acc[9];  // words 8 sl .. 8 sl + 7, and the small products' spill into the next slice
 #pragma unroll
   for (int i = 0; i < 9; i++) acc[i] = 0;
+  constexpr bool LAZY = SW >= L + 2;  // lazy partials between passes (below)
+  if (!FIRST && LAZY && active) {
+    // the earlier stripes' exact partial starts this lane's word sums (its
+    // load issues with the first index load, not after the row's shuffles):
+    // words 0..L-1 unsigned, word L+1 the signed top half of the int64 above
+    uint32_t pin[8];
+    load_slot<8>(a.part_in + (size_t)slot * SW + 8 * sl, pin, pol);
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+      acc[i] = (8 * sl + i == L + 1) ? (int64_t)(int32_t)pin[i] : (int64_t)pin[i];
+  }
   int64_t S = 0;
   const uint32_t PF = a.pf;
   const uint4* pp = a.pm_idx + si.pm_off + rw;
@@ -1079,13 +1090,11 @@ __global__ void __launch_bounds__(256, SLD_WIDE_MINB) spmv_wide(const SpmvArgs a
   // (the row bounds of mat_build), so the words above L stay below 2^48 in
   // total over the passes.  Saves one L-limb Barrett per row and pass, run by
   // one lane of T (cfg5: ~0.1 ms per extra pass).
-  constexpr bool LAZY = SW >= L + 2;
-  if (!FIRST) {
+  if (!FIRST && !LAZY) {
     uint32_t pin[SW];
     load_slot<SW>(a.part_in + (size_t)slot * SW, pin, pol);
 #pragma unroll
     for (int i = 0; i < L; i++) acc2[i] += pin[i];
-    if constexpr (LAZY) acc2[L] += (int64_t)((uint64_t)pin[L] | ((uint64_t)pin[L + 1] << 32));
   }
   if constexpr (LAZY && !LAST) {
     uint32_t o[SW];
