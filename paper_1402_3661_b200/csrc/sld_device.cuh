@@ -700,6 +700,7 @@ __global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const Sp
 #pragma unroll
   for (int i = 0; i <= L; i++) acc[i] = 0;
   int64_t S = 0;
+  // (index pipelining measured neutral here: cfg1 6.1 vs 6.0 us, 60k rows 11.96 vs 11.95 us)
   row_entries<L, 1, SHORT_K, false, 0>(a, si, kk, rw, a.x, pol, gpol, acc, S, sub);
   // the partial and the full-class entries go into other lanes' sums before
   // the reduction, so their loads overlap instead of trailing the row's tail
