@@ -176,33 +176,34 @@ def oracle_for(A):
 
 
 def cpu_sample(orc, y_limbs, target_s, log):
-    """Time the oracle port on a bounded row sample; returns (SpMV/s, cores,
-    description).  The full-vector RNS conversion (vecops to_limbs) is timed
-    separately and charged once per SpMV."""
+    """Time the oracle port on a bounded sample of one SpMV; returns
+    (SpMV/s, cores, description).  The sample is the same fraction f of the
+    SpMV's two halves, the to-RNS conversion (a window of f*ncols columns)
+    and the rows, so one SpMV = the sample's time / f (oracle spmv_sample)."""
     cores = os.cpu_count() or 1
-    N = orc.nrows
-    t = time.time()
-    orc.spmv_limbs(y_limbs, rows=(0, 0))
-    t_conv = time.time() - t
+    N, nc = orc.nrows, orc.total_cols
+    out = np.zeros((N, orc.L), dtype=np.uint32)
+    orc.spmv_sample(y_limbs, (0, 0), (0, 0), out=out)  # first call converts in full, untimed
+
+    def timed(rows):
+        cc = max(1, rows * nc // N)
+        t = time.time()
+        orc.spmv_sample(y_limbs, (0, rows), (0, cc), out=out)
+        return time.time() - t, cc
+
     rows = min(N, 2000)
     while True:
-        t = time.time()
-        orc.spmv_limbs(y_limbs, rows=(0, rows))
-        dt = time.time() - t - t_conv
+        dt, _ = timed(rows)
         if dt > 0.5 or rows >= N:
             break
         rows = min(N, rows * 4)
-    per_row = max(dt, 1e-9) / rows
     # scale the sample to ~target_s of CPU work
-    rows2 = int(min(N, max(rows, (target_s - t_conv) / per_row)))
-    t = time.time()
-    orc.spmv_limbs(y_limbs, rows=(0, rows2))
-    dt2 = time.time() - t
-    per_row = max(dt2 - t_conv, 1e-9) / rows2
-    spmv_s = t_conv + per_row * N
-    log(f"cpu oracle: {rows2} rows in {dt2:.2f}s (conversion {t_conv:.2f}s) -> {spmv_s:.3f} s/SpMV")
-    return 1.0 / spmv_s, cores, (f"oracle C port, rows [0,{rows2}) of {N} plus the full "
-                                 f"to-RNS conversion, {cores} threads, extrapolated to one SpMV")
+    rows2 = int(min(N, max(rows, target_s * rows / max(dt, 1e-9))))
+    dt2, cc2 = timed(rows2)
+    spmv_s = dt2 * N / rows2
+    log(f"cpu oracle: {rows2} rows + {cc2} columns converted in {dt2:.2f}s -> {spmv_s:.3f} s/SpMV")
+    return 1.0 / spmv_s, cores, (f"oracle C port, rows [0,{rows2}) of {N} and the to-RNS conversion "
+                                 f"of columns [0,{cc2}) of {nc}, {cores} threads, scaled to one SpMV")
 
 
 def reference_python_sample(A, mod, y_limbs, log):
@@ -231,7 +232,9 @@ def reference_python_sample(A, mod, y_limbs, log):
         pm = RM.PrimeModulus(mod.ell)
         planes = limbs_to_planes(y_limbs, RV.digit_count(mod.ell))
         t_of = {}
-        r1, r2 = min(2000, A.nrows // 4), min(8000, A.nrows)
+        # two sizes far enough apart that the per-row slope b is well above
+        # the timing noise of the conversion term a; best of 2 each
+        r1, r2 = min(2000, A.nrows // 4), min(40000, A.nrows)
         if r1 < 1 or r2 <= r1:
             return None
         for R in (r1, r2):
@@ -240,9 +243,12 @@ def reference_python_sample(A, mod, y_limbs, log):
                                 A.tags[:nz].copy(), A.small_vals[:nz].copy(),
                                 {p: v for p, v in A.full_vals.items() if p < nz}, [])
             M.kernel()  # built once per matrix, outside the per-SpMV cost
-            t = time.time()
-            RS.spmv_planes(M, planes)
-            t_of[R] = time.time() - t
+            best = None
+            for _ in range(2):
+                t = time.time()
+                RS.spmv_planes(M, planes)
+                best = min(best or 1e30, time.time() - t)
+            t_of[R] = best
         b = max(t_of[r2] - t_of[r1], 1e-9) / (r2 - r1)
         a = max(t_of[r1] - r1 * b, 0.0)
         spmv_s = a + b * A.nrows
@@ -268,26 +274,35 @@ def run_reference(args, cfg, rank, world):
     y = _random_residue_limbs(rng, A.total_cols, mod)
     cores = os.cpu_count() or 1
     N = A.nrows
-    # size each step's row sample so the whole run stays within ~2-3 minutes
-    t = time.time()
-    orc.spmv_limbs(y, rows=(0, 0))
-    t_conv = time.time() - t
-    t = time.time()
+    # each step is a bounded sample of one SpMV: the same fraction f =
+    # rows/N of its to-RNS conversion (a window of f*ncols columns) and of
+    # its rows, so one SpMV = the step's time / f with nothing subtracted.
+    # The sample is sized so the whole run stays within ~2-3 minutes.
+    nc = A.total_cols
+    out = np.zeros((N, mod.limbs), dtype=np.uint32)
+    orc.spmv_sample(y, (0, 0), (0, 0), out=out)  # first call: the full conversion, untimed
     probe = min(N, 4000)
-    orc.spmv_limbs(y, rows=(0, probe))
-    per_row = max(time.time() - t - t_conv, 1e-9) / probe
+    t = time.time()
+    orc.spmv_sample(y, (0, probe), (0, max(1, probe * nc // N)), out=out)
+    per_row = max(time.time() - t, 1e-9) / probe
     budget = 120.0 / max(1, args.steps + args.warmup)
-    rows = int(min(N, max(256, (budget - t_conv) / per_row)))
-    for _ in range(args.warmup):
-        orc.spmv_limbs(y, rows=(0, rows))
+    rows = int(min(N, max(256, budget / per_row)))
+    ccols = max(1, rows * nc // N)
+
+    def sample(k):
+        lo = (k * rows) % max(1, N - rows + 1)
+        clo = (k * ccols) % max(1, nc - ccols + 1)
+        orc.spmv_sample(y, (lo, lo + rows), (clo, clo + ccols), out=out)
+
+    for k in range(args.warmup):
+        sample(k)
     times = []
     for k in range(args.steps):
-        lo = (k * rows) % max(1, N - rows + 1)
         t = time.time()
-        orc.spmv_limbs(y, rows=(lo, lo + rows))
+        sample(k)
         times.append(time.time() - t)
     per_step = float(np.median(times))
-    spmv_s = t_conv + (per_step - t_conv) * N / rows
+    spmv_s = per_step * N / rows
     value = 1.0 / spmv_s
     ref_py = reference_python_sample(A, mod, y, log)
     line = {
@@ -298,8 +313,9 @@ def run_reference(args, cfg, rank, world):
         "data": "synthetic (native corpus generator, FFS profile, seed 1)",
         "config": config_block(args.config, cfg, A, mod, world),
         "cpu_baseline": {"value": value, "unit": "SpMV/s", "cores": cores, "kind": "port", "cpu": cpu_model(),
-                         "sample": f"{rows} rows per step of {N} (+ the full to-RNS conversion), "
-                                   f"median of {args.steps} steps, extrapolated to one SpMV"},
+                         "sample": f"{rows} rows of {N} and the to-RNS conversion of {ccols} of {nc} "
+                                   f"columns per step (the same fraction of both), median of "
+                                   f"{args.steps} steps, scaled to one SpMV"},
         "e2e": {"value": value, "unit": "SpMV/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_python": ref_py,
     }

@@ -190,6 +190,7 @@ typedef struct {
     int has_full;
     int gamma1, gamma2;
     uint64_t cmax1;
+    uint32_t *samp1, *samp2;  /* orc_spmv_sample's converted limbs */
 } orc_mat;
 
 /* build the context for headroom need = 2*gamma*cmax*l (modring.py:190-197) */
@@ -351,6 +352,7 @@ void orc_destroy(void *h) {
     if (!A) return;
     free(A->lane_ptr); free(A->lane_col); free(A->lane_tag); free(A->lane_cabs);
     free(A->full_ptr); free(A->full_col); free(A->full_val);
+    free(A->samp1); free(A->samp2);
     free(A);
 }
 
@@ -458,23 +460,69 @@ int orc_info(void *h, int64_t *out) {
  * v[r] = (A u)[r] mod l for r in [row_lo, row_hi).  u: total_cols x L words,
  * v: nrows x L words (only the requested rows are written).
  */
-int orc_spmv(void *h, const uint32_t *u, uint32_t *v, int64_t row_lo, int64_t row_hi, int nthreads) {
-    orc_mat *A = (orc_mat *)h;
+/* RnsBatch.to_limbs (vecops.py:316-319) for columns [c_lo, c_hi) */
+static void orc_to_rns(const orc_mat *A, const uint32_t *u, uint32_t *lim1, uint32_t *lim2,
+                       int64_t c_lo, int64_t c_hi) {
     const int L = A->L;
     const rns_ctx *c1 = &A->c1, *c2 = &A->c2;
     const int k1 = c1->k, k2 = A->has_full ? c2->k : 0;
-    /* RnsBatch.to_limbs (vecops.py:316-319) for every column that is read */
+#pragma omp parallel for schedule(static)
+    for (int64_t j = c_lo; j < c_hi; j++) {
+        for (int i = 0; i < k1; i++) lim1[j * k1 + i] = res_mod(u + j * L, L, c1->m[i]);
+        for (int i = 0; i < k2; i++) lim2[j * k2 + i] = res_mod(u + j * L, L, c2->m[i]);
+    }
+}
+
+static void orc_rows(const orc_mat *A, const uint32_t *lim1, const uint32_t *lim2, uint32_t *v,
+                     int64_t row_lo, int64_t row_hi);
+
+int orc_spmv(void *h, const uint32_t *u, uint32_t *v, int64_t row_lo, int64_t row_hi, int nthreads) {
+    orc_mat *A = (orc_mat *)h;
+    const int k1 = A->c1.k, k2 = A->has_full ? A->c2.k : 0;
+    /* every column that is read is converted */
     int64_t nc = A->total_cols;
     uint32_t *lim1 = (uint32_t *)malloc(8 + 4 * (size_t)k1 * nc);
     uint32_t *lim2 = k2 ? (uint32_t *)malloc(8 + 4 * (size_t)k2 * nc) : NULL;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
-#pragma omp parallel for schedule(static)
-    for (int64_t j = 0; j < nc; j++) {
-        for (int i = 0; i < k1; i++) lim1[j * k1 + i] = res_mod(u + j * L, L, c1->m[i]);
-        for (int i = 0; i < k2; i++) lim2[j * k2 + i] = res_mod(u + j * L, L, c2->m[i]);
+    orc_to_rns(A, u, lim1, lim2, 0, nc);
+    orc_rows(A, lim1, lim2, v, row_lo, row_hi);
+    free(lim1);
+    free(lim2);
+    return 0;
+}
+
+/* A bounded timing sample of one SpMV (bench.py's reference arm): the
+ * conversion of columns [c_lo, c_hi) plus rows [row_lo, row_hi), i.e. the
+ * same fraction of both halves of orc_spmv's work.  The converted limbs
+ * live in buffers kept with the matrix (converted in full on the first
+ * call), so every column a sampled row reads holds a real residue. */
+int orc_spmv_sample(void *h, const uint32_t *u, uint32_t *v, int64_t row_lo, int64_t row_hi,
+                    int64_t c_lo, int64_t c_hi, int nthreads) {
+    orc_mat *A = (orc_mat *)h;
+    const int k1 = A->c1.k, k2 = A->has_full ? A->c2.k : 0;
+    int64_t nc = A->total_cols;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    if (!A->samp1) {
+        A->samp1 = (uint32_t *)malloc(8 + 4 * (size_t)k1 * nc);
+        A->samp2 = k2 ? (uint32_t *)malloc(8 + 4 * (size_t)k2 * nc) : NULL;
+        if (!A->samp1 || (k2 && !A->samp2)) return -1;
+        orc_to_rns(A, u, A->samp1, A->samp2, 0, nc);
     }
+    if (c_lo < 0 || c_hi > nc || c_lo > c_hi || row_lo < 0 || row_hi > A->nrows || row_lo > row_hi) return -1;
+    orc_to_rns(A, u, A->samp1, A->samp2, c_lo, c_hi);
+    orc_rows(A, A->samp1, A->samp2, v, row_lo, row_hi);
+    return 0;
+}
+
+static void orc_rows(const orc_mat *A, const uint32_t *lim1, const uint32_t *lim2, uint32_t *v,
+                     int64_t row_lo, int64_t row_hi) {
+    const int L = A->L;
+    const rns_ctx *c1 = &A->c1, *c2 = &A->c2;
+    const int k1 = c1->k, k2 = A->has_full ? c2->k : 0;
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t r = row_lo; r < row_hi; r++) {
         int64_t acc[MAXK];
@@ -528,9 +576,6 @@ int orc_spmv(void *h, const uint32_t *u, uint32_t *v, int64_t row_lo, int64_t ro
         }
         reduce_compact(A, z, v + r * L);
     }
-    free(lim1);
-    free(lim2);
-    return 0;
 }
 
 /* a[t] = sum_j x[t][j] * v[j] mod l  -- DenseRows.project, solver.py:186-189

@@ -102,3 +102,22 @@ def test_oracle_dense_matvec_small():
     fvals = [rows_v for rows_v in [v for r in rows for _, v in r]]
     A = O.OracleMatrix(ell, n, n, rp, ci, tg, sv, fpos, [fvals[k] for k in fpos])
     assert A.spmv_ints(u) == want
+
+
+def test_oracle_timing_sample_matches_full_product():
+    """spmv_sample (the reference arm's bounded sample) computes the same rows
+    as the full product: first call converts every column, later calls
+    re-convert a window and compute a row range."""
+    z = O.load_golden("cfg1.npz")
+    A = O.oracle_from_fixture(z, "")
+    y = O.bytes_to_limbs(z["y"], A.L)
+    full = A.spmv_limbs(y)
+    out = np.zeros_like(full)
+    A.spmv_sample(y, (0, 0), (0, 0), out=out)
+    assert not out.any()
+    A.spmv_sample(y, (0, A.nrows), (0, A.total_cols), out=out)
+    assert np.array_equal(out, full)
+    out2 = A.spmv_sample(y, (100, 900), (5000, 6000))
+    assert np.array_equal(out2[100:900], full[100:900]) and not out2[:100].any()
+    with pytest.raises(ValueError):
+        A.spmv_sample(y, (0, A.nrows + 1), (0, 1))
