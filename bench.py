@@ -82,30 +82,67 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    every 2 ms (a 20-product cfg3 region is ~30 ms), nvidia-smi every 0.1 s
+    when NVML is unavailable.  The NVML device is found by the CUDA device's
+    PCI bus id, so CUDA_VISIBLE_DEVICES remapping cannot pick another GPU."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, power_w, reason flags x4)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        self.source = "nvidia-smi"
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(device)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            self._nvml = pynvml
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        p = self._nvml
+        sm = float(p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM))
+        r = p.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        try:
+            pw = p.nvmlDeviceGetPowerUsage(self._h) / 1000.0
+        except Exception:
+            pw = None
+        bits = [p.nvmlClocksEventReasonHwSlowdown, p.nvmlClocksEventReasonHwThermalSlowdown,
+                p.nvmlClocksEventReasonSwThermalSlowdown, p.nvmlClocksEventReasonSwPowerCap]
+        self.samples.append((sm, self._max, pw, *[bool(r & b) for b in bits]))
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        if len(f) >= 7 and f[0].replace(".", "").isdigit():
+            pw = float(f[2]) if f[2].replace(".", "").isdigit() else None
+            self.samples.append((float(f[0]), float(f[1]), pw, *[x == "Active" for x in f[3:7]]))
+
+    def _sample(self):
+        try:
+            self._sample_nvml() if self._nvml else self._sample_smi()
+        except Exception:
+            pass
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                f = [x.strip() for x in out.split(",")]
-                if len(f) >= 7:
-                    self.samples.append(f)
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+            self._sample()
+            self._stop.wait(0.002 if self._nvml else 0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -115,16 +152,18 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.samples:  # a region shorter than the first sample: take one at its end
+            self._sample()
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4) if s[3 + i]})
+        pw = sorted(s[2] for s in self.samples if s[2] is not None)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples), "source": self.source,
+                "power_w_median": pw[len(pw) // 2] if pw else None}
 
 
 def cpu_model():
