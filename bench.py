@@ -781,6 +781,20 @@ def main():
         "chain_group": group,
         "witness_check": ok_witness,
     }
+    # north_star / SURVEY 8(d) d3: the roofline is the SLOWER of the HBM-byte
+    # time and the INT32-issue time.  cfg1-cfg3 are HBM-bound (the line keeps
+    # "roofline" = HBM); where the int-op time is the longer one (cfg5's
+    # 650-bit residues) "roofline" is the int32 bound and the HBM figure moves
+    # to "hbm_roofline".
+    t_hbm = B_pass / (peak * 1e9)
+    t_int = G * int_ops(A, L) / (INT32_PEAK_TOPS * 1e12)
+    line["roofline"]["binding_time_us"] = {"hbm": t_hbm * 1e6, "int32": t_int * 1e6}
+    if t_int > t_hbm:
+        hbm = line.pop("roofline")
+        line["roofline"] = dict(line["int_roofline"], traffic=hbm["traffic"],
+                                binding_time_us=hbm["binding_time_us"],
+                                kernel=hbm["kernel"], note="int32 issue time exceeds the HBM time (SURVEY 8(d) d3)")
+        line["hbm_roofline"] = hbm
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             import oracle as O

@@ -24,11 +24,11 @@ def table():
         cpu = (d.get("cpu_baseline") or {}).get("value") or 0.0
         floor = (d.get("gather_floor") or {}).get("frac_of_floor")
         rows.append(f"| {c} ({r}) | {d['value']:.0f} | {d.get('ms_per_chain_product', d['ms_per_step']):.4f} | "
-                    f"{d['e2e']['value']:.0f} | {d['roofline']['frac']:.3f} | "
+                    f"{d['e2e']['value']:.0f} | {d['roofline']['frac']:.3f} ({d['roofline']['bound']}) | "
                     f"{floor if floor is None else f'{floor:.2f}'} | {cpu:.2f} |")
     ref, _ = latest("bench_ref_cfg3")
     out = [BEGIN,
-           "| Config | SpMV/s (device) | ms per chain-product | e2e SpMV/s | HBM roofline frac | "
+           "| Config | SpMV/s (device) | ms per chain-product | e2e SpMV/s | roofline frac (binding bound) | "
            "frac of the gather floor | CPU port SpMV/s |",
            "|---|---|---|---|---|---|---|", *rows, ""]
     if ref:
