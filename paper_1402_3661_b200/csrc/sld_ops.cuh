@@ -177,10 +177,39 @@ struct Ops {
       static const int tb = getenv("SLD_SHORT_TB") ? atoi(getenv("SLD_SHORT_TB")) : SHORT_TB;
       const unsigned grid = blocks_for(nslices * 32, tb);
       if (!grid) return true;
-      if (first && last) spmv_short<L, true, true><<<grid, tb, 0, s>>>(a, mp);
-      else if (first) spmv_short<L, true, false><<<grid, tb, 0, s>>>(a, mp);
-      else if (last) spmv_short<L, false, true><<<grid, tb, 0, s>>>(a, mp);
-      else spmv_short<L, false, false><<<grid, tb, 0, s>>>(a, mp);
+      // programmatic dependent launch: this product's CTAs become resident
+      // while the previous product drains.  Only where the whole grid fits
+      // beside the previous one, or both are multi-wave: when only part of
+      // it fits, the rest lands on the first SMs that free up and the
+      // product takes longer (20k rows 6.55 vs 6.14 us; 3k rows 4.27 vs
+      // 4.65, 60k rows 11.59 vs 12.13 with it, profiles/pdl_short_r02.txt).
+      // SLD_PDL=0 off, =1 always.
+      static const int pdl_mode = getenv("SLD_PDL") ? atoi(getenv("SLD_PDL")) : 2;
+      bool pdl = pdl_mode != 0;
+      if (pdl_mode == 2) {
+        static const int64_t cap = [] {  // resident CTAs of one grid (thread-safe init)
+          int per_sm = 0, dev = 0, sms = 0;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_short<L, true, true>, tb, 0);
+          return (int64_t)per_sm * sms;
+        }();
+        pdl = 2 * (int64_t)grid <= cap || (int64_t)grid > cap;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(tb);
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = pdl ? 1 : 0;
+      if (first && last) cudaLaunchKernelEx(&cfg, spmv_short<L, true, true>, a, mp);
+      else if (first) cudaLaunchKernelEx(&cfg, spmv_short<L, true, false>, a, mp);
+      else if (last) cudaLaunchKernelEx(&cfg, spmv_short<L, false, true>, a, mp);
+      else cudaLaunchKernelEx(&cfg, spmv_short<L, false, false>, a, mp);
       return true;
     }
     return false;
