@@ -681,7 +681,11 @@ __global__ void mk_slot_gather(const uint32_t* __restrict__ y, const int32_t* __
 constexpr int SHORT_K = 4;
 
 template <int L, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(256, spmv_min_blocks<L>()) spmv_short(const SpmvArgs a, const ModParams mp) {
+#ifndef SLD_SHORT_MAXT  // launch bounds of the short-row pass (experiment builds override)
+#define SLD_SHORT_MAXT 256
+#define SLD_SHORT_MINB spmv_min_blocks<L>()
+#endif
+__global__ void __launch_bounds__(SLD_SHORT_MAXT, SLD_SHORT_MINB) spmv_short(const SpmvArgs a, const ModParams mp) {
   constexpr int SW = stride_words(L);
   constexpr int R = 32 / SHORT_K;
   const int lane = threadIdx.x & 31;
