@@ -179,10 +179,10 @@ struct Ops {
       if (!grid) return true;
       // programmatic dependent launch: this product's CTAs become resident
       // while the previous product drains.  Only where the whole grid fits
-      // beside the previous one, or both are multi-wave: when only part of
-      // it fits, the rest lands on the first SMs that free up and the
-      // product takes longer (20k rows 6.55 vs 6.14 us; 3k rows 4.27 vs
-      // 4.65, 60k rows 11.59 vs 12.13 with it, profiles/pdl_short_r02.txt).
+      // beside the previous one, or both are multi-wave: cfg1's size (only
+      // part of the next grid fits) measured slower with it (20k rows 6.55
+      // vs 6.14 us; 3k rows 4.27 vs 4.59, 60k rows 11.61 vs 12.02 with it,
+      // profiles/pdl_short_r02.txt).
       // SLD_PDL=0 off, =1 always.
       static const int pdl_mode = getenv("SLD_PDL") ? atoi(getenv("SLD_PDL")) : 2;
       bool pdl = pdl_mode != 0;
