@@ -27,10 +27,14 @@ python tools/traffic_from_launches.py $O/launches_cfg3_g1_$TAG.csv cfg3 1 2 $O/t
 timeout 900 ncu --set full --import-source on --graph-profiling node --clock-control none -k regex:spmv_pass -s 6 -c 1 \
   -o $O/full_cfg3_g1_$TAG python tools/profile_spmv.py --config cfg3 --chains 1 --steps 4 > /dev/null 2>&1
 [ -f $O/full_cfg3_g1_$TAG.ncu-rep ] && python tools/ncu_summary.py $O/full_cfg3_g1_$TAG.ncu-rep $O/ncu_cfg3_g1_$TAG.json > /dev/null 2>&1
-# memcheck over the randomised chains and the short-row paths
-timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_stress_gpu.py -x -q \
-  -k "fresh or random_chains_vs_oracle[0] or random_chains_vs_oracle[1]" > $O/memcheck_stress_$TAG.txt 2>&1
-echo "rc=$?" >> $O/memcheck_stress_$TAG.txt
-tail -2 $O/gputests_$TAG.log; tail -1 $O/smoke_$TAG.log; tail -3 $O/memcheck_stress_$TAG.txt
+# memcheck over the randomised chains: compute-sanitizer has since been
+# closed on this pool (runs under it left GPUs needing a reset), so it is
+# attempted only when SLD_MEMCHECK=1
+if [ "${SLD_MEMCHECK:-0}" = 1 ]; then
+  timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_stress_gpu.py -x -q \
+    -k "fresh or random_chains_vs_oracle[0] or random_chains_vs_oracle[1]" > $O/memcheck_stress_$TAG.txt 2>&1
+  echo "rc=$?" >> $O/memcheck_stress_$TAG.txt
+fi
+tail -2 $O/gputests_$TAG.log; tail -1 $O/smoke_$TAG.log
 for c in cfg3 cfg2 cfg5 cfg1; do python -c "
 import json; d=json.load(open('$O/bench_${c}_$TAG.json')); print('$c', round(d['value'],1), round(d['ms_per_step'],4), d['clocks']['sm_mhz'], d['clocks']['reasons'], 'e2e', round(d['e2e']['value'],1))"; done
