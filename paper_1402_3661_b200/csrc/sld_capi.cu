@@ -15,6 +15,9 @@
 #include <string>
 #include <thread>
 #include <vector>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "sld_internal.cuh"
 
@@ -614,6 +617,37 @@ static const PackFn* pack_tab(UnpackFn** u_out) {
   return p;
 }
 
+// pack n rows into the pinned staging buffer with non-temporal stores: the
+// 16-byte streaming stores skip the read-for-ownership a cached store of a
+// fresh line costs (100 MB of extra host-memory reads at cfg3, on a path
+// bound by host memory).  Rows go through a small cached buffer; the sfence
+// makes them visible before the caller queues the DMA.  SLD_NT_STORE=0: off.
+static void pack_rows_nt(PackFn pack, const uint64_t* src, int P, uint32_t* dst, int64_t n, int L) {
+#if defined(__x86_64__)
+  static const bool nt = !getenv("SLD_NT_STORE") || atoi(getenv("SLD_NT_STORE")) != 0;
+  if (nt) {
+    int64_t r = 0;
+    while (r < n && ((uintptr_t)(dst + (size_t)r * L) & 15)) {  // up to 3 rows to a 16-byte boundary
+      pack(src + (size_t)r * P, P, dst + (size_t)r * L, 1);
+      r++;
+    }
+    if (((uintptr_t)(dst + (size_t)r * L) & 15) == 0) {
+      alignas(64) uint32_t buf[64 * MAXL];
+      for (; r + 64 <= n; r += 64) {  // 64 rows = 64 L words, a multiple of 4: stays aligned
+        pack(src + (size_t)r * P, P, buf, 64);
+        __m128i* d = (__m128i*)(dst + (size_t)r * L);
+        const __m128i* b = (const __m128i*)buf;
+        for (int i = 0; i < 16 * L; i++) _mm_stream_si128(d + i, _mm_load_si128(b + i));
+      }
+      _mm_sfence();
+    }
+    if (r < n) pack(src + (size_t)r * P, P, dst + (size_t)r * L, n - r);
+    return;
+  }
+#endif
+  pack(src, P, dst, n);
+}
+
 // rows of planes (P 16-bit digits in uint64 cells) or limbs (L words) -> device slots
 // planes of chain g at planes_g[g] (nullptr: all chains contiguous at `planes`)
 static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs, int64_t rows, int P,
@@ -639,7 +673,7 @@ static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs
     for (int64_t lo = a; lo < b; lo += SUB) {
       const int64_t hi = std::min(b, lo + SUB);
       if (planes && !planes_g) {  // one contiguous run of rows
-        pack(planes + (size_t)lo * P, P, h + (size_t)lo * L, hi - lo);
+        pack_rows_nt(pack, planes + (size_t)lo * P, P, h + (size_t)lo * L, hi - lo, L);
       } else {
         for (int64_t r = lo; r < hi; r++) {
           uint32_t* dst = h + (size_t)r * L;
