@@ -648,6 +648,35 @@ static void pack_rows_nt(PackFn pack, const uint64_t* src, int P, uint32_t* dst,
   pack(src, P, dst, n);
 }
 
+// the download's counterpart: n rows of limbs unpacked into the caller's
+// planes array (P uint64 cells per row, 3.7x the limb bytes) with streaming
+// stores, so the 374 MB written at cfg3 are not first read for ownership
+static void unpack_rows_nt(UnpackFn unpack, const uint32_t* src, uint64_t* dst, int P, int64_t n, int L) {
+#if defined(__x86_64__)
+  static const bool nt = !getenv("SLD_NT_STORE") || atoi(getenv("SLD_NT_STORE")) != 0;
+  if (nt) {
+    int64_t r = 0;
+    while (r < n && ((uintptr_t)(dst + (size_t)r * P) & 15)) {  // one row to a 16-byte boundary
+      unpack(src + (size_t)r * L, dst + (size_t)r * P, P, 1);
+      r++;
+    }
+    if (((uintptr_t)(dst + (size_t)r * P) & 15) == 0) {
+      alignas(64) uint64_t buf[32 * 2 * MAXL];
+      for (; r + 32 <= n; r += 32) {  // 32 rows = 32 P cells, an even count: stays aligned
+        unpack(src + (size_t)r * L, buf, P, 32);
+        __m128i* d = (__m128i*)(dst + (size_t)r * P);
+        const __m128i* b = (const __m128i*)buf;
+        for (int i = 0; i < 16 * P; i++) _mm_stream_si128(d + i, _mm_load_si128(b + i));
+      }
+      _mm_sfence();
+    }
+    if (r < n) unpack(src + (size_t)r * L, dst + (size_t)r * P, P, n - r);
+    return;
+  }
+#endif
+  unpack(src, dst, P, n);
+}
+
 // rows of planes (P 16-bit digits in uint64 cells) or limbs (L words) -> device slots
 // planes of chain g at planes_g[g] (nullptr: all chains contiguous at `planes`)
 static int upload_rows(sld_vec* v, const uint64_t* planes, const uint32_t* limbs, int64_t rows, int P,
@@ -733,7 +762,7 @@ static int download_rows(sld_vec* v, uint64_t* planes, uint32_t* limbs, int64_t 
       }
       const int64_t lo = k * SUB, hi = std::min(n, lo + SUB);
       if (planes && !planes_g) {
-        unpack(h + (size_t)lo * L, planes + (size_t)lo * P, P, hi - lo);
+        unpack_rows_nt(unpack, h + (size_t)lo * L, planes + (size_t)lo * P, P, hi - lo, L);
         continue;
       }
       for (int64_t r = lo; r < hi; r++) {

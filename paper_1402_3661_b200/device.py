@@ -7,6 +7,7 @@ ctypes releases the GIL for the duration of every call.
 """
 import ctypes
 import os
+import threading
 
 import numpy as np
 
@@ -14,6 +15,60 @@ from . import _native as N
 from .modring import as_modulus, ints_to_limbs, limbs_to_planes
 
 DEFAULT_DEVICE = int(os.environ.get("SLD_DEVICE", "0"))
+
+
+# ---- recycled host buffers for large downloads.  A fresh 374 MB planes
+# array (cfg3) costs ~10 ms of page faults on first touch, more than its
+# DMA and unpack.  Large outputs are therefore built on pooled buffers whose
+# pages are already mapped: each array owns a _Lease (its numpy base), and
+# when the last array or view on it dies the buffer returns to the pool.
+# Every call still returns a new array no live array shares memory with.
+_POOL_MIN_BYTES = 32 << 20
+_POOL_PER_SIZE = 2
+_pool: dict = {}
+_pool_lock = threading.Lock()
+
+
+class _Lease:
+    __slots__ = ("slab", "__weakref__")
+
+    def __init__(self, slab):
+        self.slab = slab
+
+    def __buffer__(self, flags):
+        return memoryview(self.slab)
+
+    def __release_buffer__(self, view):
+        pass
+
+    def __del__(self):
+        try:
+            with _pool_lock:
+                free = _pool.setdefault(self.slab.nbytes, [])
+                if len(free) < _POOL_PER_SIZE:
+                    free.append(self.slab)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def host_empty(shape, dtype):
+    """np.empty(shape, dtype), on a recycled buffer when it is large."""
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
+    if nbytes < _POOL_MIN_BYTES:
+        return np.empty(shape, dtype=dt)
+    with _pool_lock:
+        free = _pool.get(nbytes)
+        slab = free.pop() if free else None
+    if slab is None:
+        slab = np.empty(nbytes, dtype=np.uint8)
+    return np.frombuffer(_Lease(slab), dtype=dt).reshape(shape)
+
+
+def release_host_pool():
+    """Drop the recycled download buffers (their memory goes back to the OS)."""
+    with _pool_lock:
+        _pool.clear()
 
 
 def _dense_limbs(A, L):
@@ -122,7 +177,7 @@ class DeviceVector:
         N.check(N.load().sld_vec_upload_planes(self._h, N.ptr(p), self.n, p.shape[-1]))
 
     def download_planes(self, P):
-        out = np.empty(self._shape(P), dtype=np.uint64)
+        out = host_empty(self._shape(P), np.uint64)
         N.check(N.load().sld_vec_download_planes(self._h, N.ptr(out), self.n, P))
         return out
 
@@ -136,7 +191,7 @@ class DeviceVector:
         N.check(N.load().sld_vec_upload_planes_chains(self._h, ptrs, self.n, ps[0].shape[1]))
 
     def download_planes_list(self, P):
-        outs = [np.empty((self.n, P), dtype=np.uint64) for _ in range(self.chains)]
+        outs = [host_empty((self.n, P), np.uint64) for _ in range(self.chains)]
         ptrs = (ctypes.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
         N.check(N.load().sld_vec_download_planes_chains(self._h, ptrs, self.n, P))
         return outs
@@ -389,7 +444,7 @@ class DeviceMatrix:
         if p.shape[:-1] != lead:
             raise ValueError("plane count mismatch")
         out_shape = ((self.nrows,) if self.chains == 1 else (self.chains, self.nrows)) + (p.shape[-1],)
-        out = np.empty(out_shape, dtype=np.uint64)
+        out = host_empty(out_shape, np.uint64)
         N.check(N.load().sld_spmv_planes(self._h, N.ptr(p), N.ptr(out), p.shape[-1]))
         return out
 

@@ -107,3 +107,32 @@ def test_planted_witnesses_are_kernel_vectors():
             for c, v in w.items():
                 vec[c] = v
             assert orc.spmv_ints(vec) == [0] * A.nrows
+
+
+def test_recycled_download_buffers_never_alias_live_arrays():
+    """device.host_empty: large outputs reuse the buffer of a dead array
+    (pages already mapped) and never the memory of a live one."""
+    import gc
+
+    from paper_1402_3661_b200 import device as D
+    D.release_host_pool()
+    shape = (1 << 20, 5)  # 40 MB of uint64, above the pooling threshold
+    a = D.host_empty(shape, np.uint64)
+    assert a.shape == shape and a.dtype == np.uint64 and a.flags.writeable and a.flags.c_contiguous
+    a[:] = 7
+    b = D.host_empty(shape, np.uint64)
+    assert not np.shares_memory(a, b)
+    addr = a.ctypes.data
+    view = a[10:20]
+    del a
+    gc.collect()
+    c = D.host_empty(shape, np.uint64)  # a's buffer is still held by `view`
+    assert c.ctypes.data != addr and not np.shares_memory(c, view)
+    del view
+    gc.collect()
+    d = D.host_empty(shape, np.uint64)  # now it may come back
+    assert d.ctypes.data == addr
+    assert not np.shares_memory(d, b) and not np.shares_memory(d, c)
+    small = D.host_empty((10, 5), np.uint64)
+    assert small.shape == (10, 5) and small.flags.writeable
+    D.release_host_pool()
