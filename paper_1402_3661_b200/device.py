@@ -25,6 +25,7 @@ DEFAULT_DEVICE = int(os.environ.get("SLD_DEVICE", "0"))
 # Every call still returns a new array no live array shares memory with.
 _POOL_MIN_BYTES = 32 << 20
 _POOL_PER_SIZE = 2
+_POOL_MAX_BYTES = 1 << 30  # all pooled buffers together (kept after use)
 _pool: dict = {}
 _pool_lock = threading.Lock()
 
@@ -45,7 +46,8 @@ class _Lease:
         try:
             with _pool_lock:
                 free = _pool.setdefault(self.slab.nbytes, [])
-                if len(free) < _POOL_PER_SIZE:
+                held = sum(b.nbytes for bufs in _pool.values() for b in bufs)
+                if len(free) < _POOL_PER_SIZE and held + self.slab.nbytes <= _POOL_MAX_BYTES:
                     free.append(self.slab)
         except Exception:  # interpreter shutdown
             pass

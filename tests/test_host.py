@@ -136,3 +136,17 @@ def test_recycled_download_buffers_never_alias_live_arrays():
     small = D.host_empty((10, 5), np.uint64)
     assert small.shape == (10, 5) and small.flags.writeable
     D.release_host_pool()
+
+
+def test_recycled_buffer_pool_is_bounded(monkeypatch):
+    import gc
+
+    from paper_1402_3661_b200 import device as D
+    D.release_host_pool()
+    monkeypatch.setattr(D, "_POOL_MAX_BYTES", 50 << 20)
+    shape = (1 << 20, 5)  # 40 MB
+    a, b = D.host_empty(shape, np.uint64), D.host_empty(shape, np.uint64)
+    del a, b
+    gc.collect()
+    assert sum(x.nbytes for v in D._pool.values() for x in v) <= 50 << 20
+    D.release_host_pool()
