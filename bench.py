@@ -570,7 +570,9 @@ def main():
     v.upload_limbs(ys[0] if G == 1 else np.stack(ys))
 
     # ---- device-timed region: W untimed, then exactly K products
-    _, warm_ms = dm.bench(v, args.warmup, 0)
+    # (at least 32 products, so the per-product probe below is not a
+    # handful of first launches)
+    _, warm_ms = dm.bench(v, max(args.warmup, 32), 0)
     # per-sample events between graph launches: one sample per product pair,
     # or per 16 pairs (one 32-product graph) when a product is too short for
     # a per-pair launch not to dominate it (cfg1)

@@ -40,4 +40,9 @@ def test_repo_arm_two_ranks_folded(config):
     assert d["gpu_launches"] >= 40 and d["witness_check"] is True
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     # one sample per product pair; per 16 pairs when a product is < 0.1 ms
-    assert d["samples"]["count"] == (2 if config == "cfg1" else 20) and d["ms_per_step_median"] > 0
+    # (the probe that decides it is timed, so a rank sharing the GPU can
+    # tip it: the count must match the sample size the line states)
+    per = int(d["samples"]["per"].split()[0])
+    assert per in (2, 32) and d["samples"]["count"] == -(-40 // per) and d["ms_per_step_median"] > 0
+    if config == "cfg2":
+        assert per == 2
